@@ -1,0 +1,162 @@
+/*
+ * libmpcore — B200-native (sm_100a) DD/TD/QD dense direct solver, C ABI.
+ *
+ * Drop-in for the reference's C-ABI shared library
+ * (/root/reference/pkg/src/mpcore/build_lib.py:31-57, behaviour in
+ * /root/reference/pkg/src/mpcore/ffi.py).  The first 16 entry points below
+ * are the reference's exported symbols with identical prototypes, status
+ * codes and handle semantics; the rest are extensions (bulk planar I/O,
+ * products, device generator, profiling, distributed LU) that a foreign host
+ * needs to move n = 2048 .. 32768 systems, which the reference's
+ * one-element-at-a-time text interface cannot do.
+ *
+ * Conventions (ffi.py:1-21, build_lib.py:70-101):
+ *   - every function returns an int32 status:
+ *       0 ok, 1 invalid handle (unknown, released or wrong kind),
+ *       2 dimension/argument mismatch, NULL out-pointer or truncated buffer,
+ *       3 singular matrix, 4 parse / file error, 5 arithmetic overflow,
+ *       6 internal error (CUDA failure, or a concurrent mutation of the same
+ *         object: mutators latch their target).
+ *   - handles are sequential uint64 ids < 2^53 and are never reused;
+ *   - text crosses as NUL-terminated ASCII in caller-owned buffers,
+ *     truncated with status 2 when the buffer is too small;
+ *   - nothing unwinds across the boundary; no callbacks.
+ *   - planar layout: a k-component rows x cols object is k planes of
+ *     rows*cols binary64, row-major within each plane (simd.py:36-48).
+ * Objects live in device (HBM) memory; there is no CPU fallback: without a
+ * usable CUDA device every compute entry point returns 6 and
+ * mpcore_last_error() says why.
+ */
+#ifndef MPCORE_H
+#define MPCORE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPCORE_OK 0
+#define MPCORE_BAD_HANDLE 1
+#define MPCORE_BAD_DIMENSION 2
+#define MPCORE_SINGULAR 3
+#define MPCORE_BAD_PARSE 4
+#define MPCORE_OVERFLOW 5
+#define MPCORE_INTERNAL 6
+
+/* ---- reference ABI (build_lib.py:31-57) -------------------------------- */
+
+/* build_lib.py:32 / ffi.py:127 */
+int32_t mpcore_version(char *out, int32_t cap);
+/* build_lib.py:33 / ffi.py:131.  Mirrors MPCORE_SIMD (simd.py:17-28); the
+ * device path is the only execution path, so it selects nothing. */
+int32_t mpcore_simd_enabled(void);
+/* build_lib.py:34-35 / ffi.py:135-141: zero-filled k-component matrix */
+int32_t mpcore_matrix_new(int32_t k, int32_t rows, int32_t cols,
+                          uint64_t *out);
+/* build_lib.py:36 / ffi.py:144-149 */
+int32_t mpcore_vector_new(int32_t k, int32_t n, uint64_t *out);
+/* build_lib.py:37 / ffi.py:152-154 */
+int32_t mpcore_release(uint64_t h);
+/* build_lib.py:38-39 / ffi.py:167-186: decimal (rounded to 53k+64 bits,
+ * then to k components) or exact hex-float text; vectors use (i, 0) */
+int32_t mpcore_set_element_from_decimal(uint64_t h, int32_t i, int32_t j,
+                                        const char *text);
+/* build_lib.py:40-41 / ffi.py:189-197 */
+int32_t mpcore_get_element_components(uint64_t h, int32_t i, int32_t j,
+                                      double *out, int32_t cap);
+/* build_lib.py:42 / ffi.py:203-214: in-place P*A = L*U on the GPU; on a
+ * singular matrix returns 3 and writes 0 to *piv_out */
+int32_t mpcore_lu_factor(uint64_t h, uint64_t *piv_out);
+/* build_lib.py:43-44 / ffi.py:217-240: x <- solve(LU, piv, b) on the GPU */
+int32_t mpcore_lu_solve(uint64_t lu_h, uint64_t piv_h, uint64_t b_h,
+                        uint64_t x_h);
+/* build_lib.py:45-48 / ffi.py:243-258: load .mpmat system, run the
+ * mixed-precision iterative refinement, return a report handle */
+int32_t mpcore_refine(const char *a_path, const char *b_path,
+                      int32_t short_k, int32_t long_bits, const char *rtol,
+                      const char *atol, int32_t max_iter,
+                      uint64_t *report_out);
+/* build_lib.py:49-56 / ffi.py:266-306 */
+int32_t mpcore_report_iterations(uint64_t h, int32_t *out);
+int32_t mpcore_report_stop_reason(uint64_t h, char *out, int32_t cap);
+int32_t mpcore_report_residual_count(uint64_t h, int32_t *out);
+int32_t mpcore_report_residual_entry(uint64_t h, int32_t idx,
+                                     int32_t digits, char *out, int32_t cap);
+int32_t mpcore_report_solution_count(uint64_t h, int32_t *out);
+int32_t mpcore_report_solution_entry(uint64_t h, int32_t idx,
+                                     int32_t digits, char *out, int32_t cap);
+
+/* ---- extensions: object introspection and bulk planar transfer --------- */
+
+/* kind: 1 matrix, 2 vector, 3 pivot record, 4 report */
+int32_t mpcore_object_info(uint64_t h, int32_t *kind, int32_t *k,
+                           int32_t *rows, int32_t *cols);
+/* host planar (k*rows*cols doubles) -> device object; count must match */
+int32_t mpcore_set_planes(uint64_t h, const double *planes, int64_t count);
+/* device object -> host planar; cap in doubles */
+int32_t mpcore_get_planes(uint64_t h, double *out, int64_t cap);
+/* device-to-device copy between objects of identical shape */
+int32_t mpcore_copy(uint64_t src, uint64_t dst);
+/* pivot record from a host swap list (PivotRecord(swaps), linalg.py:348-366) */
+int32_t mpcore_pivot_new(int32_t n, const int32_t *swaps, uint64_t *out);
+/* swaps[j] = r, 0-based (linalg.py:348-354) */
+int32_t mpcore_pivot_get(uint64_t h, int32_t *out, int32_t cap);
+/* page-locked host buffers for fast H2D/D2H of planes */
+int32_t mpcore_host_alloc(int64_t bytes, void **out);
+int32_t mpcore_host_free(void *p);
+
+/* ---- extensions: compute entry points ---------------------------------- */
+
+/* lu_factor with explicit panel width (0 = default) and the singular step
+ * (SingularMatrixError.step, errors.py:21-30; -1 when nonsingular) */
+int32_t mpcore_lu_factor_ex(uint64_t h, int32_t nb, uint64_t *piv_out,
+                            int32_t *singular_step);
+/* C = A*B, mat_mul_blocked (linalg.py:577-617); C must be A.rows x B.cols */
+int32_t mpcore_mat_mul(uint64_t a, uint64_t b, uint64_t c);
+/* y = A*x, mat_vec (linalg.py:545-574) */
+int32_t mpcore_mat_vec(uint64_t a, uint64_t x, uint64_t y);
+/* out = x op y elementwise: op 0 add, 1 mul (linalg.py:648-673), 2 div
+ * (mcfloat.py:304-318; a zero divisor head returns 6) */
+int32_t mpcore_elementwise(int32_t op, uint64_t x, uint64_t y, uint64_t out);
+/* y <- y + x*alpha (axpy_batch, linalg.py:624-645); alpha: k doubles */
+int32_t mpcore_axpy(const double *alpha, int32_t k, uint64_t x, uint64_t y);
+/* fill a matrix/vector with the seeded planar recipe:
+ * slot 0 = A, 1 = B, 2 = x of a size-system_n system, seed S */
+int32_t mpcore_generate(uint64_t h, int32_t slot, int64_t system_n,
+                        uint64_t seed);
+
+/* ---- extensions: one-shot host-buffer entry points (paper names:
+ * DD/TD/QD LUdecompPM and SolveDD/TD/QDLSPM) ---------- */
+
+/* factor host planar a (k*n*n, in place) -> swaps (n int32) */
+int32_t mpcore_lu_decomp_pm(int32_t k, int32_t n, double *a_planes,
+                            int32_t *swaps, int32_t *singular_step);
+/* solve with host factors/swaps/b -> host x (k*n) */
+int32_t mpcore_solve_ls_pm(int32_t k, int32_t n, const double *lu_planes,
+                           const int32_t *swaps, const double *b_planes,
+                           double *x_planes);
+
+/* ---- extensions: device, diagnostics, profiling ------------------------ */
+
+/* select the CUDA device for this process (before any other call) */
+int32_t mpcore_set_device(int32_t device);
+int32_t mpcore_device_name(char *out, int32_t cap);
+int32_t mpcore_sm_count(int32_t *out);
+/* last error text of the calling thread */
+int32_t mpcore_last_error(char *out, int32_t cap);
+/* wait for all device work of the library stream */
+int32_t mpcore_sync(void);
+/* per-kernel-family CUDA-event timing on the library stream:
+ * slots 0 panel, 1 laswp, 2 trsm, 3 trailing update, 4 solve, 5 gemm,
+ * 6 mat_vec, 7 elementwise, 8 generator */
+int32_t mpcore_prof_enable(int32_t on);
+int32_t mpcore_prof_reset(void);
+int32_t mpcore_prof_read(double *ms, int64_t *launches, int32_t cap);
+/* FP64 issue-rate microbenchmark: DADD instructions per second */
+int32_t mpcore_fp64_peak(double *dadd_per_s, double *dfma_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPCORE_H */

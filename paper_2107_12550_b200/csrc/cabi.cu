@@ -1,0 +1,872 @@
+// libmpcore C ABI: handle table + entry points (include/mpcore.h).
+//
+// Mirrors the reference's handle-based surface (ffi.py:1-306, build_lib.py:
+// 31-208): sequential never-reused uint64 handles, a locked table, a
+// mutation latch per object (status 6 on concurrent mutation), exceptions
+// mapped to status codes, text in caller-owned buffers.  Objects hold their
+// planes in device memory; all compute runs on the library's CUDA stream.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/mpcore.h"
+#include "bignum.h"
+#include "internal.h"
+#include "refine_host.h"
+
+namespace {
+
+constexpr const char *kVersion = "0.1.0";
+
+enum Kind { K_MATRIX = 1, K_VECTOR = 2, K_PIVOT = 3, K_REPORT = 4 };
+
+struct Object {
+  int kind = 0;
+  int k = 0, rows = 0, cols = 0;
+  double *d = nullptr;          // planar device storage (matrix / vector)
+  int32_t *dswaps = nullptr;    // pivot record on device
+  std::vector<int32_t> swaps;   // pivot record on host
+  bool busy = false;            // mutation latch (ffi.py:96-105)
+  std::unique_ptr<mpr::Report> report;
+  ~Object() {
+    if (d) cudaFree(d);
+    if (dswaps) cudaFree(dswaps);
+  }
+  int64_t count() const { return (int64_t)k * rows * cols; }
+};
+using ObjPtr = std::shared_ptr<Object>;
+
+struct Table {
+  std::mutex mu;
+  uint64_t next = 1;
+  std::unordered_map<uint64_t, ObjPtr> map;
+
+  uint64_t put(ObjPtr o) {
+    std::lock_guard<std::mutex> g(mu);
+    uint64_t h = next++;
+    map[h] = std::move(o);
+    return h;
+  }
+  ObjPtr get(uint64_t h, int kind) {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = map.find(h);
+    if (it == map.end() || (kind && it->second->kind != kind)) return nullptr;
+    return it->second;
+  }
+  bool drop(uint64_t h) {
+    std::lock_guard<std::mutex> g(mu);
+    return map.erase(h) > 0;
+  }
+  // -> status; on success o is the latched object
+  int latch(uint64_t h, int kind, ObjPtr &o) {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = map.find(h);
+    if (it == map.end() || it->second->kind != kind) return MPCORE_BAD_HANDLE;
+    if (it->second->busy) return MPCORE_INTERNAL;
+    it->second->busy = true;
+    o = it->second;
+    return MPCORE_OK;
+  }
+  void unlatch(const ObjPtr &o) {
+    std::lock_guard<std::mutex> g(mu);
+    o->busy = false;
+  }
+};
+
+Table &table() {
+  static Table t;
+  return t;
+}
+
+thread_local std::string g_err;
+
+int fail(int st, const std::string &msg) {
+  g_err = msg;
+  return st;
+}
+
+// ---------------------------------------------------------------- device ----
+struct Device {
+  std::mutex mu;       // serialises device work
+  bool tried = false, ok = false;
+  int dev = -1, want = -1, sms = 0;
+  std::string why;
+  cudaStream_t stream = nullptr;
+  mpk::LuWork ws;
+};
+
+Device &device() {
+  static Device d;
+  return d;
+}
+
+int cuda_fail(cudaError_t e, const char *where) {
+  return fail(MPCORE_INTERNAL,
+              std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// -> status; initialises the device context once (lock held by caller)
+int ensure_device_locked() {
+  Device &D = device();
+  if (D.tried) return D.ok ? MPCORE_OK : fail(MPCORE_INTERNAL, D.why);
+  D.tried = true;
+  int want = D.want;
+  if (want < 0) {
+    const char *env = std::getenv("MPCORE_DEVICE");
+    if (env) want = std::atoi(env);
+  }
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    D.why = std::string("no CUDA device: ") +
+            (e != cudaSuccess ? cudaGetErrorString(e) : "count == 0");
+    return fail(MPCORE_INTERNAL, D.why);
+  }
+  if (want >= 0) {
+    e = cudaSetDevice(want);
+  } else {
+    e = cudaGetDevice(&want);
+  }
+  if (e != cudaSuccess) {
+    D.why = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
+    return fail(MPCORE_INTERNAL, D.why);
+  }
+  D.dev = want;
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, want);
+  if (prop.major < 10) {
+    D.why = std::string("device ") + prop.name +
+            " is not sm_100 class; libmpcore is built for sm_100a only";
+    return fail(MPCORE_INTERNAL, D.why);
+  }
+  D.sms = prop.multiProcessorCount;
+  e = cudaStreamCreateWithFlags(&D.stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    D.why = std::string("stream: ") + cudaGetErrorString(e);
+    return fail(MPCORE_INTERNAL, D.why);
+  }
+  mpk::LuWork &w = D.ws;
+  w.G = D.sms;
+  w.cap_w = 32;
+  w.cap_k = 4;
+  size_t rows_bytes = (size_t)2 * w.G * 32 * 4 * sizeof(double);
+  size_t rowj_bytes = (size_t)2 * 32 * 4 * sizeof(double);
+  if ((e = cudaMalloc(&w.cand_rows, rows_bytes)) != cudaSuccess ||
+      (e = cudaMalloc(&w.rowj, rowj_bytes)) != cudaSuccess ||
+      (e = cudaMalloc(&w.cand_mag, 2 * w.G * sizeof(double))) != cudaSuccess ||
+      (e = cudaMalloc(&w.cand_idx, 2 * w.G * sizeof(int32_t))) != cudaSuccess ||
+      (e = cudaMalloc(&w.bar, 2 * sizeof(unsigned))) != cudaSuccess ||
+      (e = cudaMalloc(&w.status, sizeof(int32_t))) != cudaSuccess) {
+    D.why = std::string("workspace: ") + cudaGetErrorString(e);
+    return fail(MPCORE_INTERNAL, D.why);
+  }
+  cudaMemset(w.bar, 0, 2 * sizeof(unsigned));
+  cudaMemset(w.status, 0xFF, sizeof(int32_t));
+  cudaDeviceSynchronize();
+  D.ok = true;
+  return MPCORE_OK;
+}
+
+struct DevLock {
+  std::unique_lock<std::mutex> lk;
+  int st;
+  DevLock() : lk(device().mu) { st = ensure_device_locked(); }
+};
+
+int finish(const char *where) {
+  Device &D = device();
+  cudaError_t e = cudaStreamSynchronize(D.stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, where);
+  return MPCORE_OK;
+}
+
+int copy_text(const std::string &text, char *buf, int32_t cap) {
+  if (buf == nullptr || cap <= 0) return MPCORE_BAD_DIMENSION;
+  size_t n = std::min((size_t)(cap - 1), text.size());
+  std::memcpy(buf, text.data(), n);
+  buf[n] = '\0';
+  return n == text.size() ? MPCORE_OK : MPCORE_BAD_DIMENSION;
+}
+
+mpk::MatView view(const ObjPtr &o) {
+  mpk::MatView v;
+  v.p = o->d;
+  v.ld = o->cols;
+  v.plane = (int64_t)o->rows * o->cols;
+  return v;
+}
+
+int new_container(int kind, int k, int rows, int cols, uint64_t *out) {
+  if (out == nullptr) return MPCORE_BAD_DIMENSION;
+  *out = 0;
+  if (k < 2 || k > 4 || rows < 1 || cols < 1)
+    return fail(MPCORE_BAD_DIMENSION, "bad k or shape");
+  DevLock L;
+  if (L.st) return L.st;
+  auto o = std::make_shared<Object>();
+  o->kind = kind;
+  o->k = k;
+  o->rows = rows;
+  o->cols = cols;
+  size_t bytes = (size_t)o->count() * sizeof(double);
+  cudaError_t e = cudaMalloc(&o->d, bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  e = cudaMemsetAsync(o->d, 0, bytes, device().stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemset");
+  int st = finish("matrix_new");
+  if (st) return st;
+  *out = table().put(o);
+  return MPCORE_OK;
+}
+
+ObjPtr container(uint64_t h) {
+  ObjPtr o = table().get(h, K_MATRIX);
+  if (!o) o = table().get(h, K_VECTOR);
+  return o;
+}
+
+bool locate(const ObjPtr &o, int i, int j) {
+  if (o->kind == K_MATRIX) return 0 <= i && i < o->rows && 0 <= j && j < o->cols;
+  return 0 <= i && i < o->rows * o->cols && j == 0;
+}
+
+int64_t elem_index(const ObjPtr &o, int i, int j) {
+  return o->kind == K_MATRIX ? (int64_t)i * o->cols + j : (int64_t)i;
+}
+
+int make_pivot(const std::vector<int32_t> &swaps, uint64_t *out) {
+  auto p = std::make_shared<Object>();
+  p->kind = K_PIVOT;
+  p->rows = (int)swaps.size();
+  p->cols = 1;
+  p->swaps = swaps;
+  cudaError_t e = cudaMalloc(&p->dswaps, swaps.size() * sizeof(int32_t));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(pivot)");
+  e = cudaMemcpy(p->dswaps, swaps.data(), swaps.size() * sizeof(int32_t),
+                 cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "pivot upload");
+  *out = table().put(p);
+  return MPCORE_OK;
+}
+
+int default_nb(int k, int n) {
+  (void)k;
+  (void)n;
+  return 32;
+}
+
+// factor obj in place; fills swaps; -> status (3 singular)
+int factor_locked(const ObjPtr &o, int nb, std::vector<int32_t> &swaps,
+                  int32_t *sing) {
+  Device &D = device();
+  const int n = o->rows;
+  int32_t *dsw = nullptr;
+  cudaError_t e = cudaMallocAsync(&dsw, n * sizeof(int32_t), D.stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(swaps)");
+  int32_t step = -1;
+  e = mpk::lu_factor(o->k, n, view(o), dsw, nb > 0 ? nb : default_nb(o->k, n),
+                     D.ws, &step, D.stream);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(dsw, D.stream);
+    return cuda_fail(e, "lu_factor");
+  }
+  swaps.assign(n, 0);
+  e = cudaMemcpyAsync(swaps.data(), dsw, n * sizeof(int32_t),
+                      cudaMemcpyDeviceToHost, D.stream);
+  cudaFreeAsync(dsw, D.stream);
+  int st = finish("lu_factor");
+  if (st) return st;
+  if (e != cudaSuccess) return cuda_fail(e, "swaps download");
+  if (sing) *sing = step;
+  if (step >= 0)
+    return fail(MPCORE_SINGULAR,
+                "no nonzero pivot at elimination step " + std::to_string(step));
+  return MPCORE_OK;
+}
+
+// ---------------------------------------------------------------- prof ----
+struct Prof {
+  bool on = false;
+  struct Rec { int slot; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<int> open;  // stack of indices into recs per slot
+  double ms[mpk::PROF_NSLOTS] = {0};
+  int64_t launches[mpk::PROF_NSLOTS] = {0};
+  int pending[mpk::PROF_NSLOTS];
+  Prof() { for (int &p : pending) p = -1; }
+  void collect() {
+    for (auto &r : recs) {
+      float t = 0;
+      if (cudaEventSynchronize(r.b) == cudaSuccess &&
+          cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) {
+        ms[r.slot] += t;
+        launches[r.slot] += 1;
+      }
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    recs.clear();
+  }
+};
+Prof &prof() {
+  static Prof p;
+  return p;
+}
+
+}  // namespace
+
+namespace mpk {
+void prof_begin(int slot, cudaStream_t s) {
+  Prof &P = prof();
+  if (!P.on) return;
+  Prof::Rec r;
+  r.slot = slot;
+  cudaEventCreate(&r.a);
+  cudaEventCreate(&r.b);
+  cudaEventRecord(r.a, s);
+  P.pending[slot] = (int)P.recs.size();
+  P.recs.push_back(r);
+  if (P.recs.size() > 20000) {
+    // bound the number of live events
+    cudaEventRecord(r.b, s);
+    P.pending[slot] = -1;
+    P.collect();
+  }
+}
+void prof_end(int slot, cudaStream_t s) {
+  Prof &P = prof();
+  if (!P.on || P.pending[slot] < 0) return;
+  cudaEventRecord(P.recs[P.pending[slot]].b, s);
+  P.pending[slot] = -1;
+}
+bool prof_enabled() { return prof().on; }
+int num_sms() { return device().sms > 0 ? device().sms : 148; }
+}  // namespace mpk
+
+// ================================================================= ABI ====
+extern "C" {
+
+int32_t mpcore_version(char *out, int32_t cap) {
+  return copy_text(kVersion, out, cap);
+}
+
+int32_t mpcore_simd_enabled(void) {
+  const char *v = std::getenv("MPCORE_SIMD");
+  if (!v) return 1;
+  std::string s(v);
+  size_t b = s.find_first_not_of(" \t\r\n"), e = s.find_last_not_of(" \t\r\n");
+  s = b == std::string::npos ? "" : s.substr(b, e - b + 1);
+  for (auto &c : s) c = (char)std::tolower((unsigned char)c);
+  return (s == "0" || s == "off" || s == "false" || s == "no") ? 0 : 1;
+}
+
+int32_t mpcore_matrix_new(int32_t k, int32_t rows, int32_t cols,
+                          uint64_t *out) {
+  return new_container(K_MATRIX, k, rows, cols, out);
+}
+
+int32_t mpcore_vector_new(int32_t k, int32_t n, uint64_t *out) {
+  return new_container(K_VECTOR, k, n, 1, out);
+}
+
+int32_t mpcore_release(uint64_t h) {
+  ObjPtr o = table().get(h, 0);
+  if (!o) return MPCORE_BAD_HANDLE;
+  {
+    // free device memory under the device lock (no kernel may be using it)
+    DevLock L;
+    table().drop(h);
+    o.reset();
+  }
+  return MPCORE_OK;
+}
+
+int32_t mpcore_set_element_from_decimal(uint64_t h, int32_t i, int32_t j,
+                                        const char *text) {
+  if (text == nullptr) return MPCORE_BAD_PARSE;
+  ObjPtr o = container(h);
+  if (!o) return MPCORE_BAD_HANDLE;
+  if (!locate(o, i, j)) return MPCORE_BAD_DIMENSION;
+  std::string s(text);
+  size_t b = s.find_first_not_of(" \t\r\n\f\v");
+  std::string t = b == std::string::npos ? "" : s.substr(b);
+  size_t q = t.find_first_not_of("+-");
+  bool hex = q != std::string::npos && q + 1 < t.size() && t[q] == '0' &&
+             (t[q + 1] == 'x' || t[q + 1] == 'X');
+  bn::BF v;
+  int st = hex ? bn::parse_hex(s, v) : bn::parse_decimal(s, 53 * o->k + 64, v);
+  if (st) return fail(st, "cannot parse element text");
+  double comps[4];
+  st = bn::to_multicomp(v, o->k, comps);
+  if (st) return fail(st, "element does not fit in binary64");
+  DevLock L;
+  if (L.st) return L.st;
+  int64_t idx = elem_index(o, i, j);
+  int64_t plane = (int64_t)o->rows * o->cols;
+  for (int c = 0; c < o->k; ++c) {
+    cudaError_t e = cudaMemcpyAsync(o->d + c * plane + idx, &comps[c],
+                                    sizeof(double), cudaMemcpyHostToDevice,
+                                    device().stream);
+    if (e != cudaSuccess) return cuda_fail(e, "set_element");
+  }
+  return finish("set_element");
+}
+
+int32_t mpcore_get_element_components(uint64_t h, int32_t i, int32_t j,
+                                      double *out, int32_t cap) {
+  ObjPtr o = container(h);
+  if (!o) return MPCORE_BAD_HANDLE;
+  if (!locate(o, i, j)) return MPCORE_BAD_DIMENSION;
+  if (out == nullptr || cap < o->k) return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  int64_t idx = elem_index(o, i, j);
+  int64_t plane = (int64_t)o->rows * o->cols;
+  for (int c = 0; c < o->k; ++c) {
+    cudaError_t e = cudaMemcpyAsync(&out[c], o->d + c * plane + idx,
+                                    sizeof(double), cudaMemcpyDeviceToHost,
+                                    device().stream);
+    if (e != cudaSuccess) return cuda_fail(e, "get_element");
+  }
+  return finish("get_element");
+}
+
+int32_t mpcore_lu_factor_ex(uint64_t h, int32_t nb, uint64_t *piv_out,
+                            int32_t *singular_step) {
+  if (piv_out == nullptr) return MPCORE_BAD_DIMENSION;
+  *piv_out = 0;
+  if (singular_step) *singular_step = -1;
+  ObjPtr o;
+  int st = table().latch(h, K_MATRIX, o);
+  if (st) return st;
+  struct Unlatch {
+    ObjPtr &o;
+    ~Unlatch() { table().unlatch(o); }
+  } un{o};
+  if (o->rows != o->cols)
+    return fail(MPCORE_BAD_DIMENSION, "LU needs a square matrix");
+  std::vector<int32_t> swaps;
+  {
+    DevLock L;
+    if (L.st) return L.st;
+    st = factor_locked(o, nb, swaps, singular_step);
+    if (st) return st;
+    return make_pivot(swaps, piv_out);
+  }
+}
+
+int32_t mpcore_lu_factor(uint64_t h, uint64_t *piv_out) {
+  return mpcore_lu_factor_ex(h, 0, piv_out, nullptr);
+}
+
+int32_t mpcore_lu_solve(uint64_t lu_h, uint64_t piv_h, uint64_t b_h,
+                        uint64_t x_h) {
+  ObjPtr lu = table().get(lu_h, K_MATRIX);
+  ObjPtr piv = table().get(piv_h, K_PIVOT);
+  ObjPtr b = table().get(b_h, K_VECTOR);
+  if (!lu || !piv || !b) return MPCORE_BAD_HANDLE;
+  ObjPtr x;
+  int st = table().latch(x_h, K_VECTOR, x);
+  if (st) return st;
+  struct Unlatch {
+    ObjPtr &o;
+    ~Unlatch() { table().unlatch(o); }
+  } un{x};
+  if (x->k != lu->k || b->k != lu->k) return MPCORE_BAD_DIMENSION;
+  if (piv->rows != lu->rows || x->rows != lu->rows) return MPCORE_BAD_DIMENSION;
+  if (lu->rows != lu->cols) return MPCORE_BAD_DIMENSION;
+  if (b->rows != lu->rows) return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  Device &D = device();
+  const int n = lu->rows;
+  cudaError_t e = cudaSuccess;
+  if (x->d != b->d)
+    e = cudaMemcpyAsync(x->d, b->d, (size_t)b->count() * sizeof(double),
+                        cudaMemcpyDeviceToDevice, D.stream);
+  if (e != cudaSuccess) return cuda_fail(e, "solve copy");
+  e = mpk::lu_solve(lu->k, n, view(lu), piv->dswaps, x->d, D.stream);
+  if (e != cudaSuccess) return cuda_fail(e, "lu_solve");
+  return finish("lu_solve");
+}
+
+// ------------------------------------------------------------- refine ----
+int32_t mpcore_refine(const char *a_path, const char *b_path, int32_t short_k,
+                      int32_t long_bits, const char *rtol, const char *atol,
+                      int32_t max_iter, uint64_t *report_out) {
+  if (report_out == nullptr) return MPCORE_BAD_DIMENSION;
+  *report_out = 0;
+  if (!a_path || !b_path || !rtol || !atol) return MPCORE_BAD_PARSE;
+  auto rep = std::make_unique<mpr::Report>();
+  std::string err;
+  int st = mpr::refine_files(a_path, b_path, short_k, long_bits, rtol, atol,
+                             max_iter, *rep, err);
+  if (st) return fail(st, err);
+  auto o = std::make_shared<Object>();
+  o->kind = K_REPORT;
+  o->report = std::move(rep);
+  *report_out = table().put(o);
+  return MPCORE_OK;
+}
+
+static mpr::Report *report_of(uint64_t h) {
+  ObjPtr o = table().get(h, K_REPORT);
+  return o ? o->report.get() : nullptr;
+}
+
+int32_t mpcore_report_iterations(uint64_t h, int32_t *out) {
+  mpr::Report *r = report_of(h);
+  if (!r) return MPCORE_BAD_HANDLE;
+  if (!out) return MPCORE_BAD_DIMENSION;
+  *out = r->iterations;
+  return MPCORE_OK;
+}
+
+int32_t mpcore_report_stop_reason(uint64_t h, char *out, int32_t cap) {
+  mpr::Report *r = report_of(h);
+  if (!r) return MPCORE_BAD_HANDLE;
+  return copy_text(r->stop_reason, out, cap);
+}
+
+int32_t mpcore_report_residual_count(uint64_t h, int32_t *out) {
+  mpr::Report *r = report_of(h);
+  if (!r) return MPCORE_BAD_HANDLE;
+  if (!out) return MPCORE_BAD_DIMENSION;
+  *out = (int32_t)r->residuals.size();
+  return MPCORE_OK;
+}
+
+int32_t mpcore_report_residual_entry(uint64_t h, int32_t idx, int32_t digits,
+                                     char *out, int32_t cap) {
+  mpr::Report *r = report_of(h);
+  if (!r) return MPCORE_BAD_HANDLE;
+  if (idx < 0 || idx >= (int32_t)r->residuals.size())
+    return MPCORE_BAD_DIMENSION;
+  return copy_text(mpr::format_decimal(r->residuals[idx], digits), out, cap);
+}
+
+int32_t mpcore_report_solution_count(uint64_t h, int32_t *out) {
+  mpr::Report *r = report_of(h);
+  if (!r) return MPCORE_BAD_HANDLE;
+  if (!out) return MPCORE_BAD_DIMENSION;
+  *out = (int32_t)r->solution.size();
+  return MPCORE_OK;
+}
+
+int32_t mpcore_report_solution_entry(uint64_t h, int32_t idx, int32_t digits,
+                                     char *out, int32_t cap) {
+  mpr::Report *r = report_of(h);
+  if (!r) return MPCORE_BAD_HANDLE;
+  if (idx < 0 || idx >= (int32_t)r->solution.size())
+    return MPCORE_BAD_DIMENSION;
+  return copy_text(mpr::format_decimal(r->solution[idx], digits), out, cap);
+}
+
+// --------------------------------------------------------- extensions ----
+int32_t mpcore_object_info(uint64_t h, int32_t *kind, int32_t *k,
+                           int32_t *rows, int32_t *cols) {
+  ObjPtr o = table().get(h, 0);
+  if (!o) return MPCORE_BAD_HANDLE;
+  if (kind) *kind = o->kind;
+  if (k) *k = o->k;
+  if (rows) *rows = o->rows;
+  if (cols) *cols = o->cols;
+  return MPCORE_OK;
+}
+
+int32_t mpcore_set_planes(uint64_t h, const double *planes, int64_t count) {
+  ObjPtr o;
+  int st = 0;
+  o = table().get(h, 0);
+  if (!o || (o->kind != K_MATRIX && o->kind != K_VECTOR))
+    return MPCORE_BAD_HANDLE;
+  st = table().latch(h, o->kind, o);
+  if (st) return st;
+  struct Unlatch {
+    ObjPtr &o;
+    ~Unlatch() { table().unlatch(o); }
+  } un{o};
+  if (planes == nullptr || count != o->count()) return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  cudaError_t e = cudaMemcpyAsync(o->d, planes, (size_t)count * sizeof(double),
+                                  cudaMemcpyHostToDevice, device().stream);
+  if (e != cudaSuccess) return cuda_fail(e, "set_planes");
+  return finish("set_planes");
+}
+
+int32_t mpcore_get_planes(uint64_t h, double *out, int64_t cap) {
+  ObjPtr o = container(h);
+  if (!o) return MPCORE_BAD_HANDLE;
+  if (out == nullptr || cap < o->count()) return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  cudaError_t e = cudaMemcpyAsync(out, o->d, (size_t)o->count() * sizeof(double),
+                                  cudaMemcpyDeviceToHost, device().stream);
+  if (e != cudaSuccess) return cuda_fail(e, "get_planes");
+  return finish("get_planes");
+}
+
+int32_t mpcore_copy(uint64_t src, uint64_t dst) {
+  ObjPtr s = container(src);
+  ObjPtr d = container(dst);
+  if (!s || !d) return MPCORE_BAD_HANDLE;
+  if (s->kind != d->kind || s->k != d->k || s->rows != d->rows ||
+      s->cols != d->cols)
+    return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  if (s->d == d->d) return MPCORE_OK;
+  cudaError_t e = cudaMemcpyAsync(d->d, s->d, (size_t)s->count() * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, device().stream);
+  if (e != cudaSuccess) return cuda_fail(e, "copy");
+  return finish("copy");
+}
+
+int32_t mpcore_pivot_new(int32_t n, const int32_t *swaps, uint64_t *out) {
+  if (out == nullptr) return MPCORE_BAD_DIMENSION;
+  *out = 0;
+  if (n < 1 || swaps == nullptr) return MPCORE_BAD_DIMENSION;
+  for (int j = 0; j < n; ++j)
+    if (swaps[j] < j || swaps[j] >= n)
+      return fail(MPCORE_BAD_DIMENSION, "invalid swap");
+  DevLock L;
+  if (L.st) return L.st;
+  return make_pivot(std::vector<int32_t>(swaps, swaps + n), out);
+}
+
+int32_t mpcore_pivot_get(uint64_t h, int32_t *out, int32_t cap) {
+  ObjPtr p = table().get(h, K_PIVOT);
+  if (!p) return MPCORE_BAD_HANDLE;
+  if (out == nullptr || cap < (int32_t)p->swaps.size())
+    return MPCORE_BAD_DIMENSION;
+  std::memcpy(out, p->swaps.data(), p->swaps.size() * sizeof(int32_t));
+  return MPCORE_OK;
+}
+
+int32_t mpcore_host_alloc(int64_t bytes, void **out) {
+  if (out == nullptr || bytes <= 0) return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  cudaError_t e = cudaMallocHost(out, (size_t)bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocHost");
+  return MPCORE_OK;
+}
+
+int32_t mpcore_host_free(void *p) {
+  if (p == nullptr) return MPCORE_OK;
+  cudaError_t e = cudaFreeHost(p);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFreeHost");
+  return MPCORE_OK;
+}
+
+int32_t mpcore_mat_mul(uint64_t a, uint64_t b, uint64_t c) {
+  ObjPtr A = table().get(a, K_MATRIX), B = table().get(b, K_MATRIX);
+  if (!A || !B) return MPCORE_BAD_HANDLE;
+  ObjPtr C;
+  int st = table().latch(c, K_MATRIX, C);
+  if (st) return st;
+  struct Unlatch {
+    ObjPtr &o;
+    ~Unlatch() { table().unlatch(o); }
+  } un{C};
+  if (A->k != B->k || C->k != A->k) return MPCORE_BAD_DIMENSION;
+  if (A->cols != B->rows || C->rows != A->rows || C->cols != B->cols)
+    return MPCORE_BAD_DIMENSION;
+  if (C->d == A->d || C->d == B->d)
+    return fail(MPCORE_BAD_DIMENSION, "output aliases an input");
+  DevLock L;
+  if (L.st) return L.st;
+  cudaError_t e = mpk::gemm(A->k, false, true, A->rows, B->cols, A->cols,
+                            view(A), view(B), view(C), device().stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mat_mul");
+  return finish("mat_mul");
+}
+
+int32_t mpcore_mat_vec(uint64_t a, uint64_t x, uint64_t y) {
+  ObjPtr A = table().get(a, K_MATRIX), X = table().get(x, K_VECTOR);
+  if (!A || !X) return MPCORE_BAD_HANDLE;
+  ObjPtr Y;
+  int st = table().latch(y, K_VECTOR, Y);
+  if (st) return st;
+  struct Unlatch {
+    ObjPtr &o;
+    ~Unlatch() { table().unlatch(o); }
+  } un{Y};
+  if (A->k != X->k || Y->k != A->k) return MPCORE_BAD_DIMENSION;
+  if (A->cols != X->rows || Y->rows != A->rows) return MPCORE_BAD_DIMENSION;
+  if (Y->d == X->d) return fail(MPCORE_BAD_DIMENSION, "output aliases input");
+  DevLock L;
+  if (L.st) return L.st;
+  cudaError_t e = mpk::matvec(A->k, A->rows, A->cols, view(A), X->d, Y->d,
+                              device().stream);
+  if (e != cudaSuccess) return cuda_fail(e, "mat_vec");
+  return finish("mat_vec");
+}
+
+int32_t mpcore_elementwise(int32_t op, uint64_t x, uint64_t y, uint64_t out) {
+  ObjPtr X = container(x), Y = container(y), O = container(out);
+  if (!X || !Y || !O) return MPCORE_BAD_HANDLE;
+  if (op < 0 || op > 2) return MPCORE_BAD_DIMENSION;
+  if (X->k != Y->k || O->k != X->k || X->count() != Y->count() ||
+      O->count() != X->count())
+    return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  if (op == 2) {  // division by an exact zero raises in the reference
+    std::vector<double> heads(Y->count() / Y->k);
+    cudaError_t e = cudaMemcpyAsync(heads.data(), Y->d, heads.size() * sizeof(double),
+                                    cudaMemcpyDeviceToHost, device().stream);
+    if (e != cudaSuccess) return cuda_fail(e, "div check");
+    int st = finish("div check");
+    if (st) return st;
+    for (double v : heads)
+      if (v == 0.0) return fail(MPCORE_INTERNAL, "division by zero");
+  }
+  cudaError_t e = mpk::elementwise(X->k, op, X->count() / X->k, X->d, Y->d,
+                                   O->d, device().stream);
+  if (e != cudaSuccess) return cuda_fail(e, "elementwise");
+  return finish("elementwise");
+}
+
+int32_t mpcore_axpy(const double *alpha, int32_t k, uint64_t x, uint64_t y) {
+  ObjPtr X = container(x);
+  if (!X) return MPCORE_BAD_HANDLE;
+  ObjPtr Y = container(y);
+  if (!Y) return MPCORE_BAD_HANDLE;
+  if (alpha == nullptr || k != X->k || Y->k != X->k ||
+      Y->count() != X->count())
+    return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  cudaError_t e = mpk::axpy(X->k, X->count() / X->k, alpha, X->d, Y->d,
+                            device().stream);
+  if (e != cudaSuccess) return cuda_fail(e, "axpy");
+  return finish("axpy");
+}
+
+int32_t mpcore_generate(uint64_t h, int32_t slot, int64_t system_n,
+                        uint64_t seed) {
+  ObjPtr o = container(h);
+  if (!o) return MPCORE_BAD_HANDLE;
+  if (slot < 0 || slot > 3 || system_n < 1) return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  int64_t count = (int64_t)o->rows * o->cols;
+  cudaError_t e = mpk::generate(o->k, o->d, count, count, slot, system_n, seed,
+                                device().stream);
+  if (e != cudaSuccess) return cuda_fail(e, "generate");
+  return finish("generate");
+}
+
+int32_t mpcore_lu_decomp_pm(int32_t k, int32_t n, double *a_planes,
+                            int32_t *swaps, int32_t *singular_step) {
+  if (a_planes == nullptr || swaps == nullptr) return MPCORE_BAD_DIMENSION;
+  uint64_t h = 0, piv = 0;
+  int st = mpcore_matrix_new(k, n, n, &h);
+  if (st) return st;
+  st = mpcore_set_planes(h, a_planes, (int64_t)k * n * n);
+  if (!st) st = mpcore_lu_factor_ex(h, 0, &piv, singular_step);
+  if (!st) st = mpcore_get_planes(h, a_planes, (int64_t)k * n * n);
+  if (!st) st = mpcore_pivot_get(piv, swaps, n);
+  mpcore_release(h);
+  if (piv) mpcore_release(piv);
+  return st;
+}
+
+int32_t mpcore_solve_ls_pm(int32_t k, int32_t n, const double *lu_planes,
+                           const int32_t *swaps, const double *b_planes,
+                           double *x_planes) {
+  if (!lu_planes || !swaps || !b_planes || !x_planes) return MPCORE_BAD_DIMENSION;
+  uint64_t h = 0, piv = 0, b = 0, x = 0;
+  int st = mpcore_matrix_new(k, n, n, &h);
+  if (!st) st = mpcore_set_planes(h, lu_planes, (int64_t)k * n * n);
+  if (!st) st = mpcore_pivot_new(n, swaps, &piv);
+  if (!st) st = mpcore_vector_new(k, n, &b);
+  if (!st) st = mpcore_set_planes(b, b_planes, (int64_t)k * n);
+  if (!st) st = mpcore_vector_new(k, n, &x);
+  if (!st) st = mpcore_lu_solve(h, piv, b, x);
+  if (!st) st = mpcore_get_planes(x, x_planes, (int64_t)k * n);
+  for (uint64_t hh : {h, piv, b, x})
+    if (hh) mpcore_release(hh);
+  return st;
+}
+
+int32_t mpcore_set_device(int32_t dev) {
+  Device &D = device();
+  std::lock_guard<std::mutex> g(D.mu);
+  if (D.tried) return D.dev == dev ? MPCORE_OK : fail(MPCORE_INTERNAL,
+                                                     "device already initialised");
+  D.want = dev;
+  return MPCORE_OK;
+}
+
+int32_t mpcore_device_name(char *out, int32_t cap) {
+  DevLock L;
+  if (L.st) return L.st;
+  cudaDeviceProp p;
+  cudaGetDeviceProperties(&p, device().dev);
+  return copy_text(p.name, out, cap);
+}
+
+int32_t mpcore_sm_count(int32_t *out) {
+  if (!out) return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  *out = device().sms;
+  return MPCORE_OK;
+}
+
+int32_t mpcore_last_error(char *out, int32_t cap) {
+  return copy_text(g_err, out, cap);
+}
+
+int32_t mpcore_sync(void) {
+  DevLock L;
+  if (L.st) return L.st;
+  return finish("sync");
+}
+
+int32_t mpcore_prof_enable(int32_t on) {
+  DevLock L;
+  if (L.st) return L.st;
+  prof().on = on != 0;
+  return MPCORE_OK;
+}
+
+int32_t mpcore_prof_reset(void) {
+  DevLock L;
+  if (L.st) return L.st;
+  Prof &P = prof();
+  P.collect();
+  for (int i = 0; i < mpk::PROF_NSLOTS; ++i) {
+    P.ms[i] = 0;
+    P.launches[i] = 0;
+  }
+  return MPCORE_OK;
+}
+
+int32_t mpcore_prof_read(double *ms, int64_t *launches, int32_t cap) {
+  if (!ms || !launches || cap < mpk::PROF_NSLOTS) return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  Prof &P = prof();
+  P.collect();
+  for (int i = 0; i < mpk::PROF_NSLOTS; ++i) {
+    ms[i] = P.ms[i];
+    launches[i] = P.launches[i];
+  }
+  return MPCORE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,221 @@
+// DD/TD/QD GEMM on the FP64 pipe: mat_mul_blocked (linalg.py:577-617) and
+// the LU trailing update (linalg.py:444-448 regrouped per panel).
+//
+//   C_ij <- fold over p = 0..KK-1 (ascending) of add(C_ij, mul(opA(A_ip), B_pj))
+//
+// opA = identity for mat_mul_blocked (C starts at exact +0.0, linalg.py:
+// 586-597) and opA = negation for the trailing update A22 += (-L21) U12,
+// whose chain per element continues the reference's rank-1 sequence
+// A_ic = add(A_ic, mul(-m_i, A_jc)) over the panel's steps j in ascending
+// order.  Each output element's chain is sequential in p (no split-K, no
+// Strassen) so results are bitwise those of the reference.
+//
+// Tiling: a CTA owns a BM x BN output tile; K-slices of BK are staged through
+// shared memory with cp.async (double-buffered); each thread keeps a TM x TN
+// register micro-tile of accumulators (strided over the CTA tile so shared
+// loads are broadcast / conflict-free).  The work is FP64-issue bound: per
+// madd 29 / 264 / 376 FP64 instructions (DD/TD/QD) against (TM+TN)/(TM*TN)
+// operand loads from shared memory.
+#include "internal.h"
+#include "mc.cuh"
+
+namespace mpk {
+
+namespace {
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem,
+                                          bool pred) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s),
+               "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int K, int BM, int BN, int BK, int TM, int TN>
+struct GemmCfg {
+  static constexpr int TX = BN / TN, TY = BM / TM, NT = TX * TY;
+  static constexpr int A_ELEMS = BM * BK, B_ELEMS = BK * BN;
+  static constexpr int STAGE = K * (A_ELEMS + B_ELEMS);
+  static constexpr size_t SMEM = 2 * STAGE * sizeof(double);
+};
+
+template <int K, int BM, int BN, int BK, int TM, int TN, bool NEG_A,
+          bool ZERO, int MINB>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
+gemm_kernel(int M, int N, int KK, MatView A, MatView B, MatView C,
+            const int32_t *__restrict__ status) {
+  using Cfg = GemmCfg<K, BM, BN, BK, TM, TN>;
+  constexpr int TX = Cfg::TX, TY = Cfg::TY, NT = Cfg::NT;
+  if (status != nullptr && status[0] >= 0) return;  // singular: stop
+  extern __shared__ double smem[];
+  const int tid = threadIdx.x;
+  const int tx = tid % TX, ty = tid / TX;
+  const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
+
+  auto load_tile = [&](int stage, int k0) {
+    double *As = smem + stage * Cfg::STAGE;
+    double *Bs = As + K * Cfg::A_ELEMS;
+    for (int e = tid; e < Cfg::A_ELEMS; e += NT) {
+      int r = e / BK, q = e % BK;
+      int gi = i0 + r, gq = k0 + q;
+      bool ok = gi < M && gq < KK;
+      int64_t off = ok ? (int64_t)gi * A.ld + gq : 0;
+#pragma unroll
+      for (int c = 0; c < K; ++c)
+        cp_async8(As + c * Cfg::A_ELEMS + e, A.p + c * A.plane + off, ok);
+    }
+    for (int e = tid; e < Cfg::B_ELEMS; e += NT) {
+      int q = e / BN, cc = e % BN;
+      int gq = k0 + q, gj = j0 + cc;
+      bool ok = gq < KK && gj < N;
+      int64_t off = ok ? (int64_t)gq * B.ld + gj : 0;
+#pragma unroll
+      for (int c = 0; c < K; ++c)
+        cp_async8(Bs + c * Cfg::B_ELEMS + e, B.p + c * B.plane + off, ok);
+    }
+    cp_async_commit();
+  };
+
+  double acc[TM][TN][K];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      int gi = i0 + ty + i * TY, gj = j0 + tx + j * TX;
+      bool ok = gi < M && gj < N;
+#pragma unroll
+      for (int c = 0; c < K; ++c)
+        acc[i][j][c] = (ZERO || !ok)
+                           ? 0.0
+                           : C.p[c * C.plane + (int64_t)gi * C.ld + gj];
+    }
+
+  const int ntiles = (KK + BK - 1) / BK;
+  if (ntiles > 0) load_tile(0, 0);
+  for (int kt = 0; kt < ntiles; ++kt) {
+    if (kt + 1 < ntiles) {
+      load_tile((kt + 1) & 1, (kt + 1) * BK);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double *As = smem + (kt & 1) * Cfg::STAGE;
+    const double *Bs = As + K * Cfg::A_ELEMS;
+    const int kmax = min(BK, KK - kt * BK);
+#pragma unroll 1
+    for (int kk = 0; kk < kmax; ++kk) {
+      double a[TM][K], b[TN][K];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          double v = As[c * Cfg::A_ELEMS + (ty + i * TY) * BK + kk];
+          a[i][c] = NEG_A ? -v : v;
+        }
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int c = 0; c < K; ++c)
+          b[j][c] = Bs[c * Cfg::B_ELEMS + kk * BN + tx + j * TX];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) mc::madd<K>(acc[i][j], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      int gi = i0 + ty + i * TY, gj = j0 + tx + j * TX;
+      if (gi < M && gj < N) {
+#pragma unroll
+        for (int c = 0; c < K; ++c)
+          C.p[c * C.plane + (int64_t)gi * C.ld + gj] = acc[i][j][c];
+      }
+    }
+}
+
+// Tile shapes per precision (first-cut; tuned with ncu on B200).
+template <int K> struct Tile;
+template <> struct Tile<2> {
+  static constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4, MINB = 1;
+};
+template <> struct Tile<3> {
+  static constexpr int BM = 32, BN = 32, BK = 16, TM = 2, TN = 2, MINB = 1;
+};
+template <> struct Tile<4> {
+  static constexpr int BM = 32, BN = 32, BK = 16, TM = 2, TN = 2, MINB = 1;
+};
+
+template <int K, bool NEG_A, bool ZERO>
+cudaError_t launch(int M, int N, int KK, MatView A, MatView B, MatView C,
+                   const int32_t *status, cudaStream_t s) {
+  using T = Tile<K>;
+  using Cfg = GemmCfg<K, T::BM, T::BN, T::BK, T::TM, T::TN>;
+  auto kern = gemm_kernel<K, T::BM, T::BN, T::BK, T::TM, T::TN, NEG_A, ZERO,
+                          T::MINB>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((N + T::BN - 1) / T::BN, (M + T::BM - 1) / T::BM);
+  kern<<<grid, Cfg::NT, Cfg::SMEM, s>>>(M, N, KK, A, B, C, status);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t gemm(int k, bool neg_a, bool zero_init, int M, int N, int KK,
+                 MatView A, MatView B, MatView C, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  prof_begin(PROF_GEMM, s);
+  cudaError_t e = cudaErrorInvalidValue;
+#define GEMM_CASE(KV)                                                       \
+  case KV:                                                                  \
+    if (neg_a)                                                              \
+      e = zero_init ? launch<KV, true, true>(M, N, KK, A, B, C, nullptr, s) \
+                    : launch<KV, true, false>(M, N, KK, A, B, C, nullptr, s); \
+    else                                                                    \
+      e = zero_init ? launch<KV, false, true>(M, N, KK, A, B, C, nullptr, s) \
+                    : launch<KV, false, false>(M, N, KK, A, B, C, nullptr, s); \
+    break;
+  switch (k) {
+    GEMM_CASE(2)
+    GEMM_CASE(3)
+    GEMM_CASE(4)
+    default: break;
+  }
+#undef GEMM_CASE
+  prof_end(PROF_GEMM, s);
+  return e;
+}
+
+cudaError_t lu_update(int k, int M, int N, int w, MatView L21, MatView U12,
+                      MatView A22, const int32_t *status, cudaStream_t s) {
+  if (M <= 0 || N <= 0 || w <= 0) return cudaSuccess;
+  prof_begin(PROF_UPDATE, s);
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (k) {
+    case 2: e = launch<2, true, false>(M, N, w, L21, U12, A22, status, s); break;
+    case 3: e = launch<3, true, false>(M, N, w, L21, U12, A22, status, s); break;
+    case 4: e = launch<4, true, false>(M, N, w, L21, U12, A22, status, s); break;
+    default: break;
+  }
+  prof_end(PROF_UPDATE, s);
+  return e;
+}
+
+}  // namespace mpk

@@ -1,0 +1,209 @@
+// Multi-component (DD/TD/QD) binary64 arithmetic as sm_100a device inlines.
+//
+// Every routine reproduces, operation for operation, the kernels of the
+// reference (/root/reference/pkg/src/mpcore/mcfloat.py) so results are
+// bit-identical:
+//   two_sum        mcfloat.py:55-65     (Knuth, 6 DADD)
+//   quick_two_sum  mcfloat.py:68-76     (3 DADD)
+//   two_prod       mcfloat.py:79-102    Dekker in the reference; here DMUL +
+//                                       DFMA, which yields the identical
+//                                       (p, e) pair for every operand pair
+//                                       whose product neither overflows nor
+//                                       underflows (SURVEY finding 3).
+//   sweep/cascade/compress            mcfloat.py:109-143
+//   add2/mul2/add3/mul3/add4/mul4     mcfloat.py:189-257 (term lists verbatim)
+//   mul_scalar / div                  mcfloat.py:286-318
+//
+// Every operation goes through an explicit round-to-nearest intrinsic
+// (__dadd_rn/__dmul_rn/__fma_rn), so no contraction can change a bit even if
+// the file were built without -fmad=false (the build uses it anyway).
+#pragma once
+#include <cstdint>
+
+namespace mc {
+
+#define MCI __device__ __forceinline__
+
+MCI double add_(double a, double b) { return __dadd_rn(a, b); }
+MCI double sub_(double a, double b) { return __dsub_rn(a, b); }
+MCI double mul_(double a, double b) { return __dmul_rn(a, b); }
+
+MCI void two_sum(double a, double b, double &s, double &e) {
+  s = add_(a, b);
+  double bb = sub_(s, a);
+  e = add_(sub_(a, sub_(s, bb)), sub_(b, bb));
+}
+MCI double fsum_head(double a, double b) { return add_(a, b); }
+MCI void quick_two_sum(double a, double b, double &s, double &e) {
+  s = add_(a, b);
+  e = sub_(b, sub_(s, a));
+}
+MCI void two_prod(double a, double b, double &p, double &e) {
+  p = mul_(a, b);
+  e = __fma_rn(a, b, -p);
+}
+
+// _sweep: bottom-up two_sum chain; residuals overwrite t[0..M-2].
+template <int M> MCI double sweep(double (&t)[M]) {
+  double s = t[M - 1];
+#pragma unroll
+  for (int i = M - 2; i >= 0; --i) {
+    double e;
+    two_sum(t[i], s, s, e);
+    t[i] = e;
+  }
+  return s;
+}
+// The final sweep of a cascade discards its residuals: only the running sum.
+template <int M> MCI double sweep_last(const double (&t)[M]) {
+  double s = t[M - 1];
+#pragma unroll
+  for (int i = M - 2; i >= 0; --i) s = add_(t[i], s);
+  return s;
+}
+// _cascade(terms, K) followed by _compress, for M input terms.
+template <int M, int K> struct Cascade {
+  static MCI void run(double (&t)[M], double *o) {
+    if constexpr (K == 1) {
+      o[0] = sweep_last<M>(t);
+    } else {
+      o[0] = sweep<M>(t);
+      double r[M - 1];
+#pragma unroll
+      for (int i = 0; i < M - 1; ++i) r[i] = t[i];
+      Cascade<M - 1, K - 1>::run(r, o + 1);
+    }
+  }
+};
+template <int K> MCI void compress(double *c) {
+  double carry = c[0];
+#pragma unroll
+  for (int i = 1; i < K; ++i) {
+    double s;
+    quick_two_sum(carry, c[i], s, carry);
+    c[i - 1] = s;
+  }
+  c[K - 1] = carry;
+}
+template <int M, int K> MCI void cascade_compress(double (&t)[M], double *o) {
+  Cascade<M, K>::run(t, o);
+  compress<K>(o);
+}
+
+// ------------------------------------------------------------ add / mul ----
+template <int K> struct V { double c[K]; };
+
+MCI void add2(const double *a, const double *b, double *o) {
+  double s0, e0, s1, e1;
+  two_sum(a[0], b[0], s0, e0);
+  two_sum(a[1], b[1], s1, e1);
+  e0 = add_(e0, s1);
+  quick_two_sum(s0, e0, s0, e0);
+  e0 = add_(e0, e1);
+  quick_two_sum(s0, e0, o[0], o[1]);
+}
+MCI void mul2(const double *a, const double *b, double *o) {
+  double p, e;
+  two_prod(a[0], b[0], p, e);
+  e = add_(e, add_(mul_(a[0], b[1]), mul_(a[1], b[0])));
+  quick_two_sum(p, e, o[0], o[1]);
+}
+MCI void add3(const double *a, const double *b, double *o) {
+  double s0, e0, s1, e1, s2, e2;
+  two_sum(a[0], b[0], s0, e0);
+  two_sum(a[1], b[1], s1, e1);
+  two_sum(a[2], b[2], s2, e2);
+  double t[6] = {s0, s1, e0, s2, e1, e2};
+  cascade_compress<6, 3>(t, o);
+}
+MCI void mul3(const double *a, const double *b, double *o) {
+  double p00, q00, p01, q01, p10, q10, p02, q02, p11, q11, p20, q20;
+  two_prod(a[0], b[0], p00, q00);
+  two_prod(a[0], b[1], p01, q01);
+  two_prod(a[1], b[0], p10, q10);
+  two_prod(a[0], b[2], p02, q02);
+  two_prod(a[1], b[1], p11, q11);
+  two_prod(a[2], b[0], p20, q20);
+  double t3 = add_(add_(add_(q02, q11), q20),
+                   add_(mul_(a[1], b[2]), mul_(a[2], b[1])));
+  double t[10] = {p00, p01, p10, q00, p02, p11, p20, q01, q10, t3};
+  cascade_compress<10, 3>(t, o);
+}
+MCI void add4(const double *a, const double *b, double *o) {
+  double s0, e0, s1, e1, s2, e2, s3, e3;
+  two_sum(a[0], b[0], s0, e0);
+  two_sum(a[1], b[1], s1, e1);
+  two_sum(a[2], b[2], s2, e2);
+  two_sum(a[3], b[3], s3, e3);
+  double t[8] = {s0, s1, e0, s2, e1, s3, e2, e3};
+  cascade_compress<8, 4>(t, o);
+}
+MCI void mul4(const double *a, const double *b, double *o) {
+  double p00, q00, p01, q01, p10, q10, p02, q02, p11, q11, p20, q20;
+  two_prod(a[0], b[0], p00, q00);
+  two_prod(a[0], b[1], p01, q01);
+  two_prod(a[1], b[0], p10, q10);
+  two_prod(a[0], b[2], p02, q02);
+  two_prod(a[1], b[1], p11, q11);
+  two_prod(a[2], b[0], p20, q20);
+  double t3 = add_(add_(add_(q02, q11), q20),
+                   add_(add_(mul_(a[0], b[3]), mul_(a[3], b[0])),
+                        add_(mul_(a[1], b[2]), mul_(a[2], b[1]))));
+  double t[10] = {p00, p01, p10, q00, p02, p11, p20, q01, q10, t3};
+  cascade_compress<10, 4>(t, o);
+}
+
+template <int K> MCI void add(const double *a, const double *b, double *o) {
+  if constexpr (K == 2) add2(a, b, o);
+  else if constexpr (K == 3) add3(a, b, o);
+  else add4(a, b, o);
+}
+template <int K> MCI void mul(const double *a, const double *b, double *o) {
+  if constexpr (K == 2) mul2(a, b, o);
+  else if constexpr (K == 3) mul3(a, b, o);
+  else mul4(a, b, o);
+}
+// acc <- add(acc, mul(a, b))   (the reference's madd; accumulator first)
+template <int K> MCI void madd(double *acc, const double *a, const double *b) {
+  double t[K], o[K];
+  mul<K>(a, b, t);
+  add<K>(acc, t, o);
+#pragma unroll
+  for (int c = 0; c < K; ++c) acc[c] = o[c];
+}
+// _mul_scalar_t: terms = [p_0..p_{K-1}], tails = [q_0..q_{K-1}]
+template <int K> MCI void mul_scalar(const double *a, double x, double *o) {
+  double t[2 * K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) two_prod(a[c], x, t[c], t[K + c]);
+  cascade_compress<2 * K, K>(t, o);
+}
+// _div_t: K+1 head-quotient digits of long division; b[0] != 0 required.
+template <int K> MCI void div(const double *a, const double *b, double *o) {
+  double digits[K + 1], r[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) r[c] = a[c];
+#pragma unroll
+  for (int i = 0; i < K + 1; ++i) {
+    double qi = __ddiv_rn(r[0], b[0]);
+    digits[i] = qi;
+    if (i < K) {
+      double t[K], nr[K];
+      mul_scalar<K>(b, qi, t);
+#pragma unroll
+      for (int c = 0; c < K; ++c) t[c] = -t[c];
+      add<K>(r, t, nr);
+#pragma unroll
+      for (int c = 0; c < K; ++c) r[c] = nr[c];
+    }
+  }
+  cascade_compress<K + 1, K>(digits, o);
+}
+
+// Exact FP64 instruction counts per op (FMA two_prod).
+template <int K> struct Cost;
+template <> struct Cost<2> { static constexpr int madd = 29, mul = 9, add = 20; };
+template <> struct Cost<3> { static constexpr int madd = 264, mul = 168, add = 96; };
+template <> struct Cost<4> { static constexpr int madd = 376, mul = 211, add = 165; };
+
+}  // namespace mc
