@@ -34,12 +34,14 @@ struct Object {
   int k = 0, rows = 0, cols = 0;
   double *d = nullptr;          // planar device storage (matrix / vector)
   int32_t *dswaps = nullptr;    // pivot record on device
+  int32_t *dperm = nullptr;     // composed permutation (PivotRecord.permutation)
   std::vector<int32_t> swaps;   // pivot record on host
   bool busy = false;            // mutation latch (ffi.py:96-105)
   std::unique_ptr<mpr::Report> report;
   ~Object() {
     if (d) cudaFree(d);
     if (dswaps) cudaFree(dswaps);
+    if (dperm) cudaFree(dperm);
   }
   int64_t count() const { return (int64_t)k * rows * cols; }
 };
@@ -102,6 +104,11 @@ struct Device {
   std::string why;
   cudaStream_t stream = nullptr;
   mpk::LuWork ws;
+  mpk::SolveWork sw;
+  double *tmp = nullptr;   // scratch vector (aliased solve)
+  size_t tmp_bytes = 0;
+  int32_t *dswaps = nullptr;  // LU swap output (stable for graph replay)
+  int swaps_cap = 0;
 };
 
 Device &device() {
@@ -154,24 +161,10 @@ int ensure_device_locked() {
     D.why = std::string("stream: ") + cudaGetErrorString(e);
     return fail(MPCORE_INTERNAL, D.why);
   }
-  mpk::LuWork &w = D.ws;
-  w.G = D.sms;
-  w.cap_w = 32;
-  w.cap_k = 4;
-  size_t rows_bytes = (size_t)2 * w.G * 32 * 4 * sizeof(double);
-  size_t rowj_bytes = (size_t)2 * 32 * 4 * sizeof(double);
-  if ((e = cudaMalloc(&w.cand_rows, rows_bytes)) != cudaSuccess ||
-      (e = cudaMalloc(&w.rowj, rowj_bytes)) != cudaSuccess ||
-      (e = cudaMalloc(&w.cand_mag, 2 * w.G * sizeof(double))) != cudaSuccess ||
-      (e = cudaMalloc(&w.cand_idx, 2 * w.G * sizeof(int32_t))) != cudaSuccess ||
-      (e = cudaMalloc(&w.bar, 2 * sizeof(unsigned))) != cudaSuccess ||
-      (e = cudaMalloc(&w.status, sizeof(int32_t))) != cudaSuccess) {
+  if ((e = D.ws.init(D.sms)) != cudaSuccess) {
     D.why = std::string("workspace: ") + cudaGetErrorString(e);
     return fail(MPCORE_INTERNAL, D.why);
   }
-  cudaMemset(w.bar, 0, 2 * sizeof(unsigned));
-  cudaMemset(w.status, 0xFF, sizeof(int32_t));
-  cudaDeviceSynchronize();
   D.ok = true;
   return MPCORE_OK;
 }
@@ -255,6 +248,16 @@ int make_pivot(const std::vector<int32_t> &swaps, uint64_t *out) {
   e = cudaMemcpy(p->dswaps, swaps.data(), swaps.size() * sizeof(int32_t),
                  cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "pivot upload");
+  // permutation(): position i holds original row order[i] (linalg.py:361-366)
+  std::vector<int32_t> order(swaps.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int32_t)i;
+  for (size_t j = 0; j < swaps.size(); ++j)
+    if (swaps[j] != (int32_t)j) std::swap(order[j], order[swaps[j]]);
+  e = cudaMalloc(&p->dperm, order.size() * sizeof(int32_t));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(perm)");
+  e = cudaMemcpy(p->dperm, order.data(), order.size() * sizeof(int32_t),
+                 cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "perm upload");
   *out = table().put(p);
   return MPCORE_OK;
 }
@@ -270,20 +273,24 @@ int factor_locked(const ObjPtr &o, int nb, std::vector<int32_t> &swaps,
                   int32_t *sing) {
   Device &D = device();
   const int n = o->rows;
-  int32_t *dsw = nullptr;
-  cudaError_t e = cudaMallocAsync(&dsw, n * sizeof(int32_t), D.stream);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(swaps)");
-  int32_t step = -1;
-  e = mpk::lu_factor(o->k, n, view(o), dsw, nb > 0 ? nb : default_nb(o->k, n),
-                     D.ws, &step, D.stream);
-  if (e != cudaSuccess) {
-    cudaFreeAsync(dsw, D.stream);
-    return cuda_fail(e, "lu_factor");
+  cudaError_t e;
+  // persistent swap buffer: a stable pointer lets the captured LU graph
+  // replay for every matrix of the same shape and address
+  if (D.swaps_cap < n) {
+    if (D.dswaps) cudaFree(D.dswaps);
+    D.dswaps = nullptr;
+    D.swaps_cap = 0;
+    if ((e = cudaMalloc(&D.dswaps, (size_t)n * sizeof(int32_t))) != cudaSuccess)
+      return cuda_fail(e, "cudaMalloc(swaps)");
+    D.swaps_cap = n;
   }
+  int32_t step = -1;
+  e = mpk::lu_factor(o->k, n, view(o), D.dswaps,
+                     nb > 0 ? nb : default_nb(o->k, n), D.ws, &step, D.stream);
+  if (e != cudaSuccess) return cuda_fail(e, "lu_factor");
   swaps.assign(n, 0);
-  e = cudaMemcpyAsync(swaps.data(), dsw, n * sizeof(int32_t),
+  e = cudaMemcpyAsync(swaps.data(), D.dswaps, n * sizeof(int32_t),
                       cudaMemcpyDeviceToHost, D.stream);
-  cudaFreeAsync(dsw, D.stream);
   int st = finish("lu_factor");
   if (st) return st;
   if (e != cudaSuccess) return cuda_fail(e, "swaps download");
@@ -491,11 +498,24 @@ int32_t mpcore_lu_solve(uint64_t lu_h, uint64_t piv_h, uint64_t b_h,
   Device &D = device();
   const int n = lu->rows;
   cudaError_t e = cudaSuccess;
-  if (x->d != b->d)
-    e = cudaMemcpyAsync(x->d, b->d, (size_t)b->count() * sizeof(double),
-                        cudaMemcpyDeviceToDevice, D.stream);
-  if (e != cudaSuccess) return cuda_fail(e, "solve copy");
-  e = mpk::lu_solve(lu->k, n, view(lu), piv->dswaps, x->d, D.stream);
+  const double *src = b->d;
+  if (x->d == b->d) {  // in-place solve: stage b in scratch
+    size_t bytes = (size_t)b->count() * sizeof(double);
+    if (D.tmp_bytes < bytes) {
+      if (D.tmp) cudaFree(D.tmp);
+      D.tmp = nullptr;
+      D.tmp_bytes = 0;
+      if ((e = cudaMalloc(&D.tmp, bytes)) != cudaSuccess)
+        return cuda_fail(e, "scratch");
+      D.tmp_bytes = bytes;
+    }
+    e = cudaMemcpyAsync(D.tmp, b->d, bytes, cudaMemcpyDeviceToDevice,
+                        D.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "solve copy");
+    src = D.tmp;
+  }
+  e = mpk::lu_solve(lu->k, n, view(lu), piv->dperm, src, x->d, D.sw,
+                    D.stream);
   if (e != cudaSuccess) return cuda_fail(e, "lu_solve");
   return finish("lu_solve");
 }

@@ -22,16 +22,24 @@ void prof_begin(int slot, cudaStream_t s);
 void prof_end(int slot, cudaStream_t s);
 bool prof_enabled();
 
-// Shared scratch used by the panel factorisation.
+// Shared scratch used by the panel factorisation (lu.cu).  The panel's CTAs
+// exchange per-column pivot candidates through sequence-tagged 8-byte words
+// (payload | seq, single-copy atomic), and pivot rows through plain stores
+// published by a release word; parity double-buffering keeps a slow reader's
+// step intact while fast CTAs publish the next one.
+constexpr int LU_MAX_W = 32, LU_MAX_K = 4;
+constexpr int LU_ROW_STRIDE = LU_MAX_W * LU_MAX_K + LU_MAX_K;  // row + recip
 struct LuWork {
-  double *cand_rows = nullptr;    // [2][G][W*K]
-  double *rowj = nullptr;         // [2][W*K]
-  double *cand_mag = nullptr;     // [2][G]
-  int32_t *cand_idx = nullptr;    // [2][G]
-  unsigned *bar = nullptr;        // [0] count, [1] generation
-  int32_t *status = nullptr;      // [0] singular step (or -1)
-  int G = 0;                      // CTAs of the cooperative panel launch
-  int cap_w = 0, cap_k = 0;
+  unsigned long long *cand_words = nullptr;  // [2][G][4]
+  unsigned long long *data_seq = nullptr;    // [2][G]
+  double *cand_rows = nullptr;               // [2][G][LU_ROW_STRIDE]
+  double *rowj = nullptr;                    // [2][LU_ROW_STRIDE]
+  unsigned long long *rowj_seq = nullptr;    // [2]
+  unsigned *epoch = nullptr;                 // [1] device LU call counter
+  int32_t *status = nullptr;                 // [0] singular step (or -1)
+  int G = 0;                                 // max CTAs of the panel launch
+  void *graphs = nullptr;                    // host-side graph cache
+  cudaError_t init(int sms);
 };
 
 int num_sms();
@@ -58,15 +66,27 @@ cudaError_t gemm(int k, bool neg_a, bool zero_init, int M, int N, int KK,
 // cudaSuccess; *sing_step = first singular step or -1.  nb = panel width.
 cudaError_t lu_factor(int k, int n, MatView A, int32_t *d_swaps, int nb,
                       LuWork &w, int32_t *sing_step, cudaStream_t s);
-// x (device, in: b) <- solve with LU factors and swaps
-cudaError_t lu_solve(int k, int n, MatView LU, const int32_t *d_swaps,
-                     double *x, cudaStream_t s);
+// Flags for the pipelined triangular solves (epoch-tagged, per block).
+struct SolveWork {
+  int *flags = nullptr;
+  int cap = 0;
+  int epoch = 0;
+  cudaError_t ensure(int nblk);
+  int next_epoch() { return ++epoch; }
+};
+// x <- solve(LU, perm, b): x[i] = b[perm[i]] (the reference's swaps,
+// composed), then forward and back substitution.  b and x must not alias.
+cudaError_t lu_solve(int k, int n, MatView LU, const int32_t *d_perm,
+                     const double *b, double *x, SolveWork &sw,
+                     cudaStream_t s);
 
 // panel pieces (exposed for the distributed driver)
+cudaError_t lu_begin(LuWork &ws, cudaStream_t s);
 cudaError_t lu_panel(int k, int n, MatView A, int J, int w, int32_t *d_swaps,
                      LuWork &ws, cudaStream_t s);
-cudaError_t lu_laswp(int k, int n, MatView A, int J, int w, int c0, int c1,
-                     const int32_t *d_swaps, const int32_t *status,
+// row exchanges of panel [J, J+w) on columns [c0, c1) and [c2, c3)
+cudaError_t lu_laswp(int k, MatView A, int J, int w, int c0, int c1, int c2,
+                     int c3, const int32_t *d_swaps, const int32_t *status,
                      cudaStream_t s);
 cudaError_t lu_trsm(int k, MatView L11, MatView U12, int w, int ncols,
                     const int32_t *status, cudaStream_t s);

@@ -2,22 +2,36 @@
 // reference's unblocked lane path _lu_lanes (linalg.py:422-449).
 //
 // Per panel of w columns [J, J+w):
-//   1. panel_kernel  (cooperative, one grid barrier per column): for each
-//      column j of the panel, pivot = first max of |head| over rows >= j
-//      (linalg.py:429), swap of the panel rows, singular check
-//      (linalg.py:433-436), recip = div(1, pivot) (439), multipliers
-//      m_i = mul(A_ij, recip) (441) and the rank-1 update of the remaining
-//      panel columns A_ic = add(A_ic, mul(-m_i, A_jc)) (444-448).
-//   2. laswp_kernel: the same row exchanges, in order, on every column
+//   1. panel_kernel (cooperative): for each column j of the panel, pivot =
+//      first max of |head| over rows >= j (linalg.py:429), swap of the panel
+//      rows, singular check (433-436), recip = div(1, pivot) (439),
+//      multipliers m_i = mul(A_ij, recip) (441) and the rank-1 update of the
+//      remaining panel columns A_ic = add(A_ic, mul(-m_i, A_jc)) (444-448).
+//   2. laswp_kernel: the same row exchanges, composed, on every column
 //      outside the panel (the reference swaps full rows, 430-431).
 //   3. trsm_kernel: U12 rows J..J+w-1 of the trailing columns, continuing
-//      each element's chain with the panel steps it had not seen yet
-//      (ascending j, so each element sees exactly the reference's chain).
+//      each element's chain with the panel steps it had not seen yet.
 //   4. lu_update (gemm.cu): A22 <- fold_j add(A22, mul(-L21_ij, U12_jc)).
-// Every element of the matrix therefore sees the same sequence of
-// add(., mul(-m, u)) operations, in the same order, as in the reference;
-// blocking changes only when each link is executed (SURVEY finding 2).
+// Every element sees the same sequence of add(., mul(-m, u)) operations, in
+// the same order, as in the reference; blocking only changes when each link
+// runs (SURVEY finding 2).
+//
+// Panel protocol (per column, no grid barrier): every CTA owns a contiguous
+// slice of the panel's rows in shared memory.  For column j each CTA
+//   (a) publishes its local first-max candidate (row, |head|) as three
+//       sequence-tagged 8-byte words, right after updating column j;
+//   (b) finishes the rank-1 update of the remaining panel columns while a
+//       spare warp computes div(1, candidate pivot) speculatively, then
+//       publishes its candidate row + reciprocal behind a release word;
+//   (c) polls all candidate words (one L2 round trip), takes the global
+//       first max, and reads the winner's row and reciprocal.
+// The speculative reciprocal of the winner is exactly the reference's
+// recip = div(1, pivot), so nothing changes bitwise; its latency and the
+// bulk update overlap the candidate exchange.
 #include <climits>
+#include <cstdlib>
+#include <vector>
+
 #include "internal.h"
 #include "mc.cuh"
 
@@ -27,29 +41,24 @@ namespace {
 
 constexpr int PANEL_THREADS = 256;
 constexpr int NWARPS = PANEL_THREADS / 32;
+typedef unsigned long long u64;
 
-__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned nblocks) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned *vgen = bar + 1;
-    unsigned gen = *vgen;
-    __threadfence();
-    unsigned arrived = atomicAdd(bar, 1u);
-    if (arrived == nblocks - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*vgen == gen) {
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
+__device__ __forceinline__ void st_volatile(u64 *p, u64 v) {
+  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v)
+               : "memory");
+}
+__device__ __forceinline__ u64 ld_volatile(const u64 *p) {
+  u64 v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ u64 ll_word(unsigned payload, unsigned seq) {
+  return ((u64)payload << 32) | seq;
 }
 
-// (mag, row) ordering: larger magnitude wins; ties go to the smaller row
-// (np.argmax returns the first maximum).
+// (mag, row): larger magnitude wins; ties go to the smaller row
+// (np.argmax returns the first maximum, linalg.py:429).
 __device__ __forceinline__ bool better(double m1, int r1, double m2, int r2) {
   return m1 > m2 || (m1 == m2 && r1 < r2);
 }
@@ -74,98 +83,161 @@ __device__ __forceinline__ void block_argmax(double &mag, int &row,
       int orow = __shfl_down_sync(0xffffffffu, row, off);
       if (better(om, orow, mag, row)) { mag = om; row = orow; }
     }
-    if (lane == 0) { s_mag[0] = mag; s_row[0] = row; }
+    if (lane == 0) { s_mag[NWARPS] = mag; s_row[NWARPS] = row; }
   }
   __syncthreads();
-  mag = s_mag[0];
-  row = s_row[0];
-  __syncthreads();
+  mag = s_mag[NWARPS];
+  row = s_row[NWARPS];
 }
 
-// Panel factorisation over rows [J, n), columns [J, J+w).  CTA g keeps rows
-// [J + g*R, J + (g+1)*R) of the panel resident in shared memory.
+struct PanelShared {
+  double s_mag[NWARPS + 1];
+  int s_row[NWARPS + 1];
+  double spec_recip[LU_MAX_K];
+  int cand_row;        // local candidate (global row index) of the next step
+  int winner;          // winning row of the current step
+};
+
 template <int K, int W>
 __global__ void __launch_bounds__(PANEL_THREADS, 1)
 panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
              LuWork ws) {
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
   if (ws.status[0] >= 0) return;
+  // sequence numbers: unique per LU call (device epoch) and column
+  const unsigned seq0 = ws.epoch[0] * 65536u + (unsigned)J + 1u;
   const int m = n - J;
   const int R = (m + G - 1) / G;
   const int rbeg = J + g * R;
   const int nr = max(0, min(rbeg + R, n) - rbeg);
   extern __shared__ double sm[];
-  double *rows = sm;                 // [R][W][K]
-  double *prow = rows + R * W * K;   // [W][K]
-  double *recip = prow + W * K;      // [K]
-  __shared__ double s_mag[NWARPS];
-  __shared__ int s_row[NWARPS];
+  double *rows = sm;                  // [R][W][K]
+  double *prow = rows + R * W * K;    // [W][K] pivot row of this step
+  double *recip = prow + W * K;       // [K]
+  __shared__ PanelShared S;
+
+  auto at = [&](int r, int col) -> double * { return rows + (r * W + col) * K; };
 
   for (int e = tid; e < nr * w; e += PANEL_THREADS) {
     int r = e / w, col = e % w;
 #pragma unroll
     for (int c = 0; c < K; ++c)
-      rows[(r * W + col) * K + c] =
-          A.p[c * A.plane + (int64_t)(rbeg + r) * A.ld + J + col];
+      at(r, col)[c] = A.p[c * A.plane + (int64_t)(rbeg + r) * A.ld + J + col];
   }
   __syncthreads();
 
-  for (int jj = 0; jj < w; ++jj) {
-    const int j = J + jj, par = jj & 1;
+  // local candidate over column jj (rows >= j), published as LL words
+  auto publish_candidate = [&](int jj, unsigned seq) {
+    const int j = J + jj;
     double mag = -1.0;
     int row = INT_MAX;
     for (int r = tid; r < nr; r += PANEL_THREADS) {
       int gi = rbeg + r;
       if (gi >= j) {
-        double v = fabs(rows[(r * W + jj) * K]);
+        double v = fabs(at(r, jj)[0]);
         if (better(v, gi, mag, row)) { mag = v; row = gi; }
       }
     }
-    block_argmax(mag, row, s_mag, s_row);
-    // publish this CTA's candidate row (and row j if owned)
-    double *cand = ws.cand_rows + ((int64_t)par * G + g) * (W * K);
-    if (row != INT_MAX) {
-      int r = row - rbeg;
-      for (int e = tid; e < w * K; e += PANEL_THREADS)
-        cand[e] = rows[r * W * K + e];
-    }
-    if (j >= rbeg && j < rbeg + nr) {
-      int r = j - rbeg;
-      double *rj = ws.rowj + (int64_t)par * (W * K);
-      for (int e = tid; e < w * K; e += PANEL_THREADS) rj[e] = rows[r * W * K + e];
-    }
+    block_argmax(mag, row, S.s_mag, S.s_row);
     if (tid == 0) {
-      ws.cand_mag[par * G + g] = mag;
-      ws.cand_idx[par * G + g] = row;
+      S.cand_row = row;
+      u64 *wd = ws.cand_words + ((int64_t)(jj & 1) * G + g) * 4;
+      unsigned long long mb = __double_as_longlong(mag);
+      st_volatile(wd + 0, ll_word((unsigned)row, seq));
+      st_volatile(wd + 1, ll_word((unsigned)(mb & 0xffffffffu), seq));
+      st_volatile(wd + 2, ll_word((unsigned)(mb >> 32), seq));
     }
-    grid_sync(ws.bar, G);
-    // global first-max over the published candidates
-    double gm = -1.0;
-    int gr = INT_MAX, gw = 0;
-    for (int t = tid; t < G; t += PANEL_THREADS) {
-      double cm = __ldcg(ws.cand_mag + par * G + t);
-      int cr = __ldcg(ws.cand_idx + par * G + t);
-      if (better(cm, cr, gm, gr)) { gm = cm; gr = cr; }
-    }
-    block_argmax(gm, gr, s_mag, s_row);
-    const int r = gr;
-    // the winner CTA is the owner of row r
-    gw = (r - J) / R;
-    const double *wrow = ws.cand_rows + ((int64_t)par * G + gw) * (W * K);
-    for (int e = tid; e < w * K; e += PANEL_THREADS) prow[e] = __ldcg(wrow + e);
     __syncthreads();
-    if (r != j) {
-      if (r >= rbeg && r < rbeg + nr) {
-        const double *rj = ws.rowj + (int64_t)par * (W * K);
-        int lr = r - rbeg;
-        for (int e = tid; e < w * K; e += PANEL_THREADS)
-          rows[lr * W * K + e] = __ldcg(rj + e);
+  };
+  // speculative reciprocal of the local candidate's pivot (one thread)
+  auto spec_div = [&](int jj) {
+    int row = S.cand_row;
+    if (row != INT_MAX) {
+      double one[K], pv[K], q[K];
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        one[c] = c == 0 ? 1.0 : 0.0;
+        pv[c] = at(row - rbeg, jj)[c];
       }
-      if (j >= rbeg && j < rbeg + nr) {
-        int lr = j - rbeg;
-        for (int e = tid; e < w * K; e += PANEL_THREADS)
-          rows[lr * W * K + e] = prow[e];
+      mc::div<K>(one, pv, q);
+#pragma unroll
+      for (int c = 0; c < K; ++c) S.spec_recip[c] = q[c];
+    }
+  };
+  // candidate row + recip (and row j if owned), then the release word
+  auto publish_data = [&](int jj, unsigned seq) {
+    const int j = J + jj, par = jj & 1;
+    const int row = S.cand_row;
+    double *dst = ws.cand_rows + ((int64_t)par * G + g) * LU_ROW_STRIDE;
+    if (row != INT_MAX) {
+      const double *src = at(row - rbeg, 0);
+      for (int e = tid; e < w * K; e += PANEL_THREADS) dst[e] = src[e];
+      if (tid < K) dst[W * K + tid] = S.spec_recip[tid];
+    }
+    const bool own_j = j >= rbeg && j < rbeg + nr;
+    if (own_j) {
+      double *rj = ws.rowj + (int64_t)par * LU_ROW_STRIDE;
+      const double *src = at(j - rbeg, 0);
+      for (int e = tid; e < w * K; e += PANEL_THREADS) rj[e] = src[e];
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      st_volatile(ws.data_seq + par * G + g, (u64)seq);
+      if (own_j) st_volatile(ws.rowj_seq + par, (u64)seq);
+    }
+  };
+
+  // prologue: column 0
+  publish_candidate(0, seq0);
+  if (tid == 0) spec_div(0);
+  __syncthreads();
+  publish_data(0, seq0);
+
+  for (int jj = 0; jj < w; ++jj) {
+    const int j = J + jj, par = jj & 1;
+    const unsigned seq = seq0 + jj;
+    // (c) global first max over the published candidates
+    double gm = -1.0;
+    int gr = INT_MAX;
+    if (tid < G) {
+      const u64 *wd = ws.cand_words + ((int64_t)par * G + tid) * 4;
+      u64 a, b, c;
+      do {
+        a = ld_volatile(wd + 0);
+        b = ld_volatile(wd + 1);
+        c = ld_volatile(wd + 2);
+      } while ((unsigned)a != seq || (unsigned)b != seq || (unsigned)c != seq);
+      gr = (int)(a >> 32);
+      gm = __longlong_as_double((long long)((b >> 32) | ((c >> 32) << 32)));
+    }
+    block_argmax(gm, gr, S.s_mag, S.s_row);
+    const int r = gr;
+    const int gw = (r - J) / R;
+    const bool own_r = r >= rbeg && r < rbeg + nr;
+    const bool own_j = j >= rbeg && j < rbeg + nr;
+    if (tid == 0) {
+      while (ld_volatile(ws.data_seq + par * G + gw) != (u64)seq) {
       }
+      if (r != j && own_r) {
+        while (ld_volatile(ws.rowj_seq + par) != (u64)seq) {
+        }
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    const double *wrow = ws.cand_rows + ((int64_t)par * G + gw) * LU_ROW_STRIDE;
+    for (int e = tid; e < w * K; e += PANEL_THREADS) prow[e] = __ldcg(wrow + e);
+    if (tid < K) recip[tid] = __ldcg(wrow + W * K + tid);
+    if (r != j && own_r) {
+      const double *rj = ws.rowj + (int64_t)par * LU_ROW_STRIDE;
+      double *dst = at(r - rbeg, 0);
+      for (int e = tid; e < w * K; e += PANEL_THREADS) dst[e] = __ldcg(rj + e);
+    }
+    __syncthreads();
+    if (r != j && own_j) {
+      double *dst = at(j - rbeg, 0);
+      for (int e = tid; e < w * K; e += PANEL_THREADS) dst[e] = prow[e];
     }
     if (g == 0 && tid == 0) swaps[j] = r;
     if (prow[jj * K] == 0.0) {  // singular at step j (uniform decision)
@@ -173,83 +245,121 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       return;
     }
     if (j == n - 1) break;  // linalg.py:437-438: no reciprocal at the end
-    if (tid == 0) {
-      double one[K], pv[K], q[K];
-#pragma unroll
-      for (int c = 0; c < K; ++c) {
-        one[c] = c == 0 ? 1.0 : 0.0;
-        pv[c] = prow[jj * K + c];
-      }
-      mc::div<K>(one, pv, q);
-#pragma unroll
-      for (int c = 0; c < K; ++c) recip[c] = q[c];
-    }
     __syncthreads();
-    // multipliers m_i = mul(A_ij, recip)
+    // multipliers m_i = mul(A_ij, recip) for local rows i > j
     for (int rr = tid; rr < nr; rr += PANEL_THREADS) {
       if (rbeg + rr > j) {
         double a[K], rc[K], o[K];
 #pragma unroll
         for (int c = 0; c < K; ++c) {
-          a[c] = rows[(rr * W + jj) * K + c];
+          a[c] = at(rr, jj)[c];
           rc[c] = recip[c];
         }
         mc::mul<K>(a, rc, o);
 #pragma unroll
-        for (int c = 0; c < K; ++c) rows[(rr * W + jj) * K + c] = o[c];
+        for (int c = 0; c < K; ++c) at(rr, jj)[c] = o[c];
       }
     }
     __syncthreads();
-    // rank-1 update of the remaining panel columns
-    const int ncol = w - jj - 1;
-    for (int e = tid; e < nr * ncol; e += PANEL_THREADS) {
-      int rr = e / ncol, cc = jj + 1 + e % ncol;
+    if (jj + 1 >= w) break;
+    // look-ahead: column jj+1 first
+    for (int rr = tid; rr < nr; rr += PANEL_THREADS) {
       if (rbeg + rr > j) {
         double negm[K], u[K], acc[K];
 #pragma unroll
         for (int c = 0; c < K; ++c) {
-          negm[c] = -rows[(rr * W + jj) * K + c];
-          u[c] = prow[cc * K + c];
-          acc[c] = rows[(rr * W + cc) * K + c];
+          negm[c] = -at(rr, jj)[c];
+          u[c] = prow[(jj + 1) * K + c];
+          acc[c] = at(rr, jj + 1)[c];
         }
         mc::madd<K>(acc, negm, u);
 #pragma unroll
-        for (int c = 0; c < K; ++c) rows[(rr * W + cc) * K + c] = acc[c];
+        for (int c = 0; c < K; ++c) at(rr, jj + 1)[c] = acc[c];
       }
     }
     __syncthreads();
+    publish_candidate(jj + 1, seq + 1);
+    // remaining columns (warps 1..) while lane 0 of warp 0 divides
+    if (tid == 0) {
+      spec_div(jj + 1);
+    } else if (tid >= 32) {
+      const int ncol = w - jj - 2;
+      for (int e = tid - 32; e < nr * ncol; e += PANEL_THREADS - 32) {
+        int rr = e / ncol, cc = jj + 2 + e % ncol;
+        if (rbeg + rr > j) {
+          double negm[K], u[K], acc[K];
+#pragma unroll
+          for (int c = 0; c < K; ++c) {
+            negm[c] = -at(rr, jj)[c];
+            u[c] = prow[cc * K + c];
+            acc[c] = at(rr, cc)[c];
+          }
+          mc::madd<K>(acc, negm, u);
+#pragma unroll
+          for (int c = 0; c < K; ++c) at(rr, cc)[c] = acc[c];
+        }
+      }
+    }
+    __syncthreads();
+    publish_data(jj + 1, seq + 1);
   }
 
   for (int e = tid; e < nr * w; e += PANEL_THREADS) {
     int r = e / w, col = e % w;
 #pragma unroll
     for (int c = 0; c < K; ++c)
-      A.p[c * A.plane + (int64_t)(rbeg + r) * A.ld + J + col] =
-          rows[(r * W + col) * K + c];
+      A.p[c * A.plane + (int64_t)(rbeg + r) * A.ld + J + col] = at(r, col)[c];
   }
 }
 
-// Row exchanges of panel [J, J+w) applied in order to columns [c0, c1) and
-// [c2, c3) (everything outside the panel).  One thread per (column, plane).
+__global__ void lu_begin_kernel(unsigned *epoch, int32_t *status) {
+  epoch[0] += 1u;
+  status[0] = -1;
+}
+
+// Row exchanges of panel [J, J+w), composed once per CTA in shared memory:
+// after the swaps, row cur[i] holds what row src[i] held before.  Each
+// thread then moves one column (of one plane): all loads, then all stores.
 template <int K>
-__global__ void laswp_kernel(MatView A, int J, int w, int c0, int c1, int c2,
-                             int c3, const int32_t *__restrict__ swaps,
-                             const int32_t *__restrict__ status) {
+__global__ void __launch_bounds__(256)
+laswp_kernel(MatView A, int J, int w, int c0, int c1, int c2, int c3,
+             const int32_t *__restrict__ swaps,
+             const int32_t *__restrict__ status) {
   if (status[0] >= 0) return;
+  __shared__ int cur[2 * LU_MAX_W], src[2 * LU_MAX_W];
+  __shared__ int cnt;
+  if (threadIdx.x == 0) {
+    int m = 0;
+    for (int jj = 0; jj < w; ++jj) {
+      int a = J + jj, b = swaps[a];
+      if (a == b) continue;
+      int ia = -1, ib = -1;
+      for (int t = 0; t < m; ++t) {
+        if (cur[t] == a) ia = t;
+        if (cur[t] == b) ib = t;
+      }
+      if (ia < 0) { cur[m] = a; src[m] = a; ia = m++; }
+      if (ib < 0) { cur[m] = b; src[m] = b; ib = m++; }
+      int t = src[ia]; src[ia] = src[ib]; src[ib] = t;
+    }
+    cnt = m;
+  }
+  __syncthreads();
+  const int m = cnt;
+  if (m == 0) return;
   const int n1 = c1 - c0, n2 = c3 - c2, ncols = n1 + n2;
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= ncols * K) return;
   int c = t / ncols, q = t % ncols;
   int col = q < n1 ? c0 + q : c2 + (q - n1);
   double *p = A.p + c * A.plane + col;
-  for (int jj = 0; jj < w; ++jj) {
-    int j = J + jj, r = swaps[j];
-    if (r != j) {
-      double a = p[(int64_t)j * A.ld], b = p[(int64_t)r * A.ld];
-      p[(int64_t)j * A.ld] = b;
-      p[(int64_t)r * A.ld] = a;
-    }
-  }
+  double v[2 * LU_MAX_W];
+#pragma unroll
+  for (int i = 0; i < 2 * LU_MAX_W; ++i)
+    if (i < m) v[i] = p[(int64_t)src[i] * A.ld];
+#pragma unroll
+  for (int i = 0; i < 2 * LU_MAX_W; ++i)
+    if (i < m) p[(int64_t)cur[i] * A.ld] = v[i];
 }
 
 // U12 = panel rows [J, J+w) of the trailing columns.  Thread (jj, cl) owns
@@ -302,6 +412,22 @@ trsm_kernel(MatView L11, MatView U12, int w, int ncols,
   }
 }
 
+template <typename... KArgs, typename... Args>
+cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block,
+                        size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int K, int W>
 size_t panel_smem(int R) {
   return ((size_t)R * W * K + W * K + K) * sizeof(double);
@@ -315,14 +441,15 @@ cudaError_t panel_k(int n, MatView A, int J, int w, int32_t *d_swaps,
   const int R = (m + G - 1) / G;
   size_t smem = panel_smem<K, W>(R);
   auto kern = panel_kernel<K, W>;
-  cudaError_t e = cudaFuncSetAttribute(
-      kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  LuWork wcopy = ws;
-  void *args[] = {(void *)&n, (void *)&A, (void *)&J, (void *)&w,
-                  (void *)&d_swaps, (void *)&wcopy};
-  return cudaLaunchCooperativeKernel((const void *)kern, dim3(G),
-                                     dim3(PANEL_THREADS), args, smem, s);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  return launch_coop(kern, dim3(G), dim3(PANEL_THREADS), smem, s, n, A, J, w,
+                     d_swaps, ws);
 }
 
 template <int K, int W>
@@ -334,7 +461,84 @@ cudaError_t trsm_k(MatView L11, MatView U12, int w, int ncols,
   return cudaGetLastError();
 }
 
+MatView sub(MatView A, int i, int j) {
+  MatView v = A;
+  v.p = A.p + (int64_t)i * A.ld + j;
+  return v;
+}
+
+// -------------------------------------------------------- graph cache ----
+struct GraphKey {
+  const double *p;
+  int64_t ld, plane;
+  int k, n, nb;
+  const int32_t *swaps;
+  bool operator==(const GraphKey &o) const {
+    return p == o.p && ld == o.ld && plane == o.plane && k == o.k &&
+           n == o.n && nb == o.nb && swaps == o.swaps;
+  }
+};
+struct GraphCache {
+  struct Entry {
+    GraphKey key;
+    cudaGraphExec_t exec;
+  };
+  std::vector<Entry> entries;
+};
+
+cudaError_t enqueue_lu(int k, int n, MatView A, int32_t *d_swaps, int nb,
+                       LuWork &ws, cudaStream_t s) {
+  cudaError_t e;
+  if ((e = lu_begin(ws, s)) != cudaSuccess) return e;
+  for (int J = 0; J < n; J += nb) {
+    const int w = min(nb, n - J);
+    if ((e = lu_panel(k, n, A, J, w, d_swaps, ws, s)) != cudaSuccess) return e;
+    if ((e = lu_laswp(k, A, J, w, 0, J, J + w, n, d_swaps, ws.status, s)) !=
+        cudaSuccess)
+      return e;
+    const int rest = n - J - w;
+    if (rest > 0) {
+      if ((e = lu_trsm(k, sub(A, J, J), sub(A, J, J + w), w, rest, ws.status,
+                       s)) != cudaSuccess)
+        return e;
+      if ((e = lu_update(k, rest, rest, w, sub(A, J + w, J), sub(A, J, J + w),
+                         sub(A, J + w, J + w), ws.status, s)) != cudaSuccess)
+        return e;
+    }
+  }
+  return cudaSuccess;
+}
+
 }  // namespace
+
+cudaError_t LuWork::init(int sms) {
+  G = sms;
+  cudaError_t e;
+  size_t words = (size_t)2 * G * 4 * sizeof(u64);
+  if ((e = cudaMalloc(&cand_words, words)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&data_seq, 2 * G * sizeof(u64))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&cand_rows, (size_t)2 * G * LU_ROW_STRIDE *
+                                      sizeof(double))) != cudaSuccess)
+    return e;
+  if ((e = cudaMalloc(&rowj, 2 * LU_ROW_STRIDE * sizeof(double))) !=
+      cudaSuccess)
+    return e;
+  if ((e = cudaMalloc(&rowj_seq, 2 * sizeof(u64))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&epoch, sizeof(unsigned))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&status, sizeof(int32_t))) != cudaSuccess) return e;
+  cudaMemset(cand_words, 0, words);
+  cudaMemset(data_seq, 0, 2 * G * sizeof(u64));
+  cudaMemset(rowj_seq, 0, 2 * sizeof(u64));
+  cudaMemset(epoch, 0, sizeof(unsigned));
+  cudaMemset(status, 0xFF, sizeof(int32_t));
+  graphs = new GraphCache();
+  return cudaDeviceSynchronize();
+}
+
+cudaError_t lu_begin(LuWork &ws, cudaStream_t s) {
+  lu_begin_kernel<<<1, 1, 0, s>>>(ws.epoch, ws.status);
+  return cudaGetLastError();
+}
 
 cudaError_t lu_panel(int k, int n, MatView A, int J, int w, int32_t *d_swaps,
                      LuWork &ws, cudaStream_t s) {
@@ -357,20 +561,17 @@ cudaError_t lu_panel(int k, int n, MatView A, int J, int w, int32_t *d_swaps,
   return e;
 }
 
-cudaError_t lu_laswp(int k, int n, MatView A, int J, int w, int c0, int c1,
-                     const int32_t *d_swaps, const int32_t *status,
+cudaError_t lu_laswp(int k, MatView A, int J, int w, int c0, int c1, int c2,
+                     int c3, const int32_t *d_swaps, const int32_t *status,
                      cudaStream_t s) {
-  // columns [0, J) and [J+w, n)
-  (void)c0; (void)c1;
-  int ncols = J + (n - J - w);
+  int ncols = (c1 - c0) + (c3 - c2);
   if (ncols <= 0) return cudaSuccess;
   prof_begin(PROF_LASWP, s);
-  int total = ncols * k;
-  int blocks = (total + 255) / 256;
+  int blocks = (ncols * k + 255) / 256;
   switch (k) {
-    case 2: laswp_kernel<2><<<blocks, 256, 0, s>>>(A, J, w, 0, J, J + w, n, d_swaps, status); break;
-    case 3: laswp_kernel<3><<<blocks, 256, 0, s>>>(A, J, w, 0, J, J + w, n, d_swaps, status); break;
-    case 4: laswp_kernel<4><<<blocks, 256, 0, s>>>(A, J, w, 0, J, J + w, n, d_swaps, status); break;
+    case 2: laswp_kernel<2><<<blocks, 256, 0, s>>>(A, J, w, c0, c1, c2, c3, d_swaps, status); break;
+    case 3: laswp_kernel<3><<<blocks, 256, 0, s>>>(A, J, w, c0, c1, c2, c3, d_swaps, status); break;
+    case 4: laswp_kernel<4><<<blocks, 256, 0, s>>>(A, J, w, c0, c1, c2, c3, d_swaps, status); break;
     default: return cudaErrorInvalidValue;
   }
   prof_end(PROF_LASWP, s);
@@ -399,36 +600,40 @@ cudaError_t lu_trsm(int k, MatView L11, MatView U12, int w, int ncols,
   return e;
 }
 
-static MatView sub(MatView A, int i, int j) {
-  MatView v = A;
-  v.p = A.p + (int64_t)i * A.ld + j;
-  return v;
-}
-
 cudaError_t lu_factor(int k, int n, MatView A, int32_t *d_swaps, int nb,
                       LuWork &ws, int32_t *sing_step, cudaStream_t s) {
   cudaError_t e;
-  if (nb > 32) nb = 32;
+  if (nb > LU_MAX_W) nb = LU_MAX_W;
   if (nb < 1) nb = 1;
-  e = cudaMemsetAsync(ws.status, 0xFF, sizeof(int32_t), s);  // -1
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(ws.bar, 0, 2 * sizeof(unsigned), s);
-  if (e != cudaSuccess) return e;
-  for (int J = 0; J < n; J += nb) {
-    const int w = min(nb, n - J);
-    if ((e = lu_panel(k, n, A, J, w, d_swaps, ws, s)) != cudaSuccess) return e;
-    if ((e = lu_laswp(k, n, A, J, w, 0, 0, d_swaps, ws.status, s)) !=
-        cudaSuccess)
-      return e;
-    const int rest = n - J - w;
-    if (rest > 0) {
-      if ((e = lu_trsm(k, sub(A, J, J), sub(A, J, J + w), w, rest, ws.status,
-                       s)) != cudaSuccess)
+  static const bool no_graph = std::getenv("MPCORE_NO_GRAPH") != nullptr;
+  if (prof_enabled() || no_graph) {
+    // direct launches (per-kernel event timing needs them)
+    if ((e = enqueue_lu(k, n, A, d_swaps, nb, ws, s)) != cudaSuccess) return e;
+  } else {
+    GraphCache &gc = *static_cast<GraphCache *>(ws.graphs);
+    GraphKey key{A.p, A.ld, A.plane, k, n, nb, d_swaps};
+    cudaGraphExec_t exec = nullptr;
+    for (auto &en : gc.entries)
+      if (en.key == key) exec = en.exec;
+    if (!exec) {
+      cudaGraph_t graph;
+      if ((e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal)) !=
+          cudaSuccess)
         return e;
-      if ((e = lu_update(k, rest, rest, w, sub(A, J + w, J), sub(A, J, J + w),
-                         sub(A, J + w, J + w), ws.status, s)) != cudaSuccess)
-        return e;
+      cudaError_t ee = enqueue_lu(k, n, A, d_swaps, nb, ws, s);
+      e = cudaStreamEndCapture(s, &graph);
+      if (ee != cudaSuccess) return ee;
+      if (e != cudaSuccess) return e;
+      e = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) return e;
+      if (gc.entries.size() >= 16) {
+        cudaGraphExecDestroy(gc.entries.front().exec);
+        gc.entries.erase(gc.entries.begin());
+      }
+      gc.entries.push_back({key, exec});
     }
+    if ((e = cudaGraphLaunch(exec, s)) != cudaSuccess) return e;
   }
   e = cudaMemcpyAsync(sing_step, ws.status, sizeof(int32_t),
                       cudaMemcpyDeviceToHost, s);
