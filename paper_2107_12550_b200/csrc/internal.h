@@ -28,13 +28,12 @@ bool prof_enabled();
 // published by a release word; parity double-buffering keeps a slow reader's
 // step intact while fast CTAs publish the next one.
 constexpr int LU_MAX_W = 32, LU_MAX_K = 4;
-constexpr int LU_ROW_STRIDE = LU_MAX_W * LU_MAX_K + LU_MAX_K;  // row + recip
+constexpr int LU_CAND_WORDS = 16;                    // idx, mag(2), pivot(2K)
+constexpr int LU_ROW_WORDS = 2 * LU_MAX_W * LU_MAX_K;  // a panel row, 2/double
 struct LuWork {
-  unsigned long long *cand_words = nullptr;  // [2][G][4]
-  unsigned long long *data_seq = nullptr;    // [2][G]
-  double *cand_rows = nullptr;               // [2][G][LU_ROW_STRIDE]
-  double *rowj = nullptr;                    // [2][LU_ROW_STRIDE]
-  unsigned long long *rowj_seq = nullptr;    // [2]
+  unsigned long long *cand_words = nullptr;  // [2][G][LU_CAND_WORDS]
+  unsigned long long *row_words = nullptr;   // [2][G][LU_ROW_WORDS]
+  unsigned long long *rowj_words = nullptr;  // [2][LU_ROW_WORDS]
   unsigned *epoch = nullptr;                 // [1] device LU call counter
   int32_t *status = nullptr;                 // [0] singular step (or -1)
   int G = 0;                                 // max CTAs of the panel launch

@@ -16,18 +16,22 @@
 // the same order, as in the reference; blocking only changes when each link
 // runs (SURVEY finding 2).
 //
-// Panel protocol (per column, no grid barrier): every CTA owns a contiguous
-// slice of the panel's rows in shared memory.  For column j each CTA
-//   (a) publishes its local first-max candidate (row, |head|) as three
-//       sequence-tagged 8-byte words, right after updating column j;
-//   (b) finishes the rank-1 update of the remaining panel columns while a
-//       spare warp computes div(1, candidate pivot) speculatively, then
-//       publishes its candidate row + reciprocal behind a release word;
-//   (c) polls all candidate words (one L2 round trip), takes the global
-//       first max, and reads the winner's row and reciprocal.
-// The speculative reciprocal of the winner is exactly the reference's
-// recip = div(1, pivot), so nothing changes bitwise; its latency and the
-// bulk update overlap the candidate exchange.
+// Panel protocol (per column, no grid barrier, no memory fences): every
+// CTA owns a contiguous slice of the panel's rows in shared memory, and all
+// cross-CTA data travels as self-validating 8-byte words (32-bit payload |
+// 32-bit sequence number; aligned 8-byte accesses are single-copy atomic).
+// For column j each CTA
+//   (a) updates column j first (look-ahead), then publishes its local
+//       first-max candidate: row index, |head| and the pivot value;
+//   (b) finishes the rank-1 update of the remaining panel columns and
+//       publishes its candidate row (and row j, if it owns it);
+//   (c) polls every CTA's candidate words (one L2 round trip), takes the
+//       global first max, computes recip = div(1, pivot) from the winner's
+//       words (every CTA the same bits) while its other warps stream in the
+//       winner's row, and applies the swap.
+// Sequence numbers are unique per (LU call, column) and the word buffers are
+// double-buffered by column parity, so a slow CTA's step is never
+// overwritten before it has been consumed.
 #include <climits>
 #include <cstdlib>
 #include <vector>
@@ -93,10 +97,17 @@ __device__ __forceinline__ void block_argmax(double &mag, int &row,
 struct PanelShared {
   double s_mag[NWARPS + 1];
   int s_row[NWARPS + 1];
-  double spec_recip[LU_MAX_K];
-  int cand_row;        // local candidate (global row index) of the next step
-  int winner;          // winning row of the current step
+  double recip[LU_MAX_K];
+  int cand_row;        // local candidate (global row index) of the step
 };
+
+// LL word helpers: a double travels as two words (low half, high half)
+__device__ __forceinline__ unsigned lo32(double v) {
+  return (unsigned)((unsigned long long)__double_as_longlong(v) & 0xffffffffu);
+}
+__device__ __forceinline__ unsigned hi32(double v) {
+  return (unsigned)((unsigned long long)__double_as_longlong(v) >> 32);
+}
 
 template <int K, int W>
 __global__ void __launch_bounds__(PANEL_THREADS, 1)
@@ -110,10 +121,10 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
   const int R = (m + G - 1) / G;
   const int rbeg = J + g * R;
   const int nr = max(0, min(rbeg + R, n) - rbeg);
+  const int rw = 2 * w * K;  // LL words per panel row
   extern __shared__ double sm[];
   double *rows = sm;                  // [R][W][K]
   double *prow = rows + R * W * K;    // [W][K] pivot row of this step
-  double *recip = prow + W * K;       // [K]
   __shared__ PanelShared S;
 
   auto at = [&](int r, int col) -> double * { return rows + (r * W + col) * K; };
@@ -126,7 +137,8 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
   }
   __syncthreads();
 
-  // local candidate over column jj (rows >= j), published as LL words
+  // (a) local first-max candidate of column jj; words: idx, |head| (2),
+  //     pivot value (2K) -- self-validating, no fence needed
   auto publish_candidate = [&](int jj, unsigned seq) {
     const int j = J + jj;
     double mag = -1.0;
@@ -139,100 +151,104 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       }
     }
     block_argmax(mag, row, S.s_mag, S.s_row);
+    u64 *wd = ws.cand_words + ((int64_t)(jj & 1) * G + g) * LU_CAND_WORDS;
     if (tid == 0) {
       S.cand_row = row;
-      u64 *wd = ws.cand_words + ((int64_t)(jj & 1) * G + g) * 4;
-      unsigned long long mb = __double_as_longlong(mag);
       st_volatile(wd + 0, ll_word((unsigned)row, seq));
-      st_volatile(wd + 1, ll_word((unsigned)(mb & 0xffffffffu), seq));
-      st_volatile(wd + 2, ll_word((unsigned)(mb >> 32), seq));
-    }
-    __syncthreads();
-  };
-  // speculative reciprocal of the local candidate's pivot (one thread)
-  auto spec_div = [&](int jj) {
-    int row = S.cand_row;
-    if (row != INT_MAX) {
-      double one[K], pv[K], q[K];
-#pragma unroll
-      for (int c = 0; c < K; ++c) {
-        one[c] = c == 0 ? 1.0 : 0.0;
-        pv[c] = at(row - rbeg, jj)[c];
-      }
-      mc::div<K>(one, pv, q);
-#pragma unroll
-      for (int c = 0; c < K; ++c) S.spec_recip[c] = q[c];
+      st_volatile(wd + 1, ll_word(lo32(mag), seq));
+      st_volatile(wd + 2, ll_word(hi32(mag), seq));
+    } else if (tid <= 2 * K && row != INT_MAX) {
+      const double v = at(row - rbeg, jj)[(tid - 1) >> 1];
+      st_volatile(wd + 2 + tid, ll_word((tid & 1) ? lo32(v) : hi32(v), seq));
     }
   };
-  // candidate row + recip (and row j if owned), then the release word
-  auto publish_data = [&](int jj, unsigned seq) {
+  // (b) candidate row and (if owned) row j, once every column is current
+  auto publish_rows = [&](int jj, unsigned seq) {
     const int j = J + jj, par = jj & 1;
     const int row = S.cand_row;
-    double *dst = ws.cand_rows + ((int64_t)par * G + g) * LU_ROW_STRIDE;
     if (row != INT_MAX) {
+      u64 *wd = ws.row_words + ((int64_t)par * G + g) * LU_ROW_WORDS;
       const double *src = at(row - rbeg, 0);
-      for (int e = tid; e < w * K; e += PANEL_THREADS) dst[e] = src[e];
-      if (tid < K) dst[W * K + tid] = S.spec_recip[tid];
+      for (int e = tid; e < rw; e += PANEL_THREADS) {
+        double v = src[e >> 1];
+        st_volatile(wd + e, ll_word((e & 1) ? hi32(v) : lo32(v), seq));
+      }
     }
-    const bool own_j = j >= rbeg && j < rbeg + nr;
-    if (own_j) {
-      double *rj = ws.rowj + (int64_t)par * LU_ROW_STRIDE;
+    if (j >= rbeg && j < rbeg + nr) {
+      u64 *wd = ws.rowj_words + (int64_t)par * LU_ROW_WORDS;
       const double *src = at(j - rbeg, 0);
-      for (int e = tid; e < w * K; e += PANEL_THREADS) rj[e] = src[e];
-    }
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-      st_volatile(ws.data_seq + par * G + g, (u64)seq);
-      if (own_j) st_volatile(ws.rowj_seq + par, (u64)seq);
+      for (int e = tid; e < rw; e += PANEL_THREADS) {
+        double v = src[e >> 1];
+        st_volatile(wd + e, ll_word((e & 1) ? hi32(v) : lo32(v), seq));
+      }
     }
   };
+  // poll one LL word until it carries `seq`; return its payload
+  auto poll = [](const u64 *p, unsigned seq) -> unsigned {
+    u64 v;
+    do {
+      v = ld_volatile(p);
+    } while ((unsigned)v != seq);
+    return (unsigned)(v >> 32);
+  };
 
-  // prologue: column 0
   publish_candidate(0, seq0);
-  if (tid == 0) spec_div(0);
   __syncthreads();
-  publish_data(0, seq0);
+  publish_rows(0, seq0);
 
   for (int jj = 0; jj < w; ++jj) {
     const int j = J + jj, par = jj & 1;
     const unsigned seq = seq0 + jj;
-    // (c) global first max over the published candidates
+    // (c) global first max over all candidates: one L2 round trip
     double gm = -1.0;
     int gr = INT_MAX;
     if (tid < G) {
-      const u64 *wd = ws.cand_words + ((int64_t)par * G + tid) * 4;
-      u64 a, b, c;
-      do {
-        a = ld_volatile(wd + 0);
-        b = ld_volatile(wd + 1);
-        c = ld_volatile(wd + 2);
-      } while ((unsigned)a != seq || (unsigned)b != seq || (unsigned)c != seq);
-      gr = (int)(a >> 32);
-      gm = __longlong_as_double((long long)((b >> 32) | ((c >> 32) << 32)));
+      const u64 *wd = ws.cand_words + ((int64_t)par * G + tid) * LU_CAND_WORDS;
+      unsigned a = poll(wd + 0, seq);
+      unsigned b = poll(wd + 1, seq);
+      unsigned c = poll(wd + 2, seq);
+      gr = (int)a;
+      gm = __longlong_as_double((long long)(((u64)c << 32) | b));
     }
     block_argmax(gm, gr, S.s_mag, S.s_row);
     const int r = gr;
     const int gw = (r - J) / R;
     const bool own_r = r >= rbeg && r < rbeg + nr;
     const bool own_j = j >= rbeg && j < rbeg + nr;
-    if (tid == 0) {
-      while (ld_volatile(ws.data_seq + par * G + gw) != (u64)seq) {
-      }
-      if (r != j && own_r) {
-        while (ld_volatile(ws.rowj_seq + par) != (u64)seq) {
+    const bool last = (j == n - 1);
+    // warp 0: pivot value -> recip = div(1, pivot) (every CTA, same bits);
+    // other warps: the winner's pivot row (and row j for the new owner of r)
+    if (tid < 32) {
+      if (!last) {
+        const u64 *wd = ws.cand_words + ((int64_t)par * G + gw) * LU_CAND_WORDS;
+        unsigned half = tid < 2 * K ? poll(wd + 3 + tid, seq) : 0u;
+        double pv[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          unsigned l = __shfl_sync(0xffffffffu, half, 2 * c);
+          unsigned h = __shfl_sync(0xffffffffu, half, 2 * c + 1);
+          pv[c] = __longlong_as_double((long long)(((u64)h << 32) | l));
+        }
+        if (tid == 0 && pv[0] != 0.0) {
+          double one[K], q[K];
+#pragma unroll
+          for (int c = 0; c < K; ++c) one[c] = c == 0 ? 1.0 : 0.0;
+          mc::div<K>(one, pv, q);
+#pragma unroll
+          for (int c = 0; c < K; ++c) S.recip[c] = q[c];
         }
       }
-      __threadfence();
-    }
-    __syncthreads();
-    const double *wrow = ws.cand_rows + ((int64_t)par * G + gw) * LU_ROW_STRIDE;
-    for (int e = tid; e < w * K; e += PANEL_THREADS) prow[e] = __ldcg(wrow + e);
-    if (tid < K) recip[tid] = __ldcg(wrow + W * K + tid);
-    if (r != j && own_r) {
-      const double *rj = ws.rowj + (int64_t)par * LU_ROW_STRIDE;
-      double *dst = at(r - rbeg, 0);
-      for (int e = tid; e < w * K; e += PANEL_THREADS) dst[e] = __ldcg(rj + e);
+    } else {
+      const u64 *wd = ws.row_words + ((int64_t)par * G + gw) * LU_ROW_WORDS;
+      unsigned *pr = reinterpret_cast<unsigned *>(prow);
+      for (int e = tid - 32; e < rw; e += PANEL_THREADS - 32)
+        pr[e] = poll(wd + e, seq);
+      if (r != j && own_r) {
+        const u64 *wj = ws.rowj_words + (int64_t)par * LU_ROW_WORDS;
+        unsigned *dst = reinterpret_cast<unsigned *>(at(r - rbeg, 0));
+        for (int e = tid - 32; e < rw; e += PANEL_THREADS - 32)
+          dst[e] = poll(wj + e, seq);
+      }
     }
     __syncthreads();
     if (r != j && own_j) {
@@ -244,7 +260,7 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       if (g == 0 && tid == 0) ws.status[0] = j;
       return;
     }
-    if (j == n - 1) break;  // linalg.py:437-438: no reciprocal at the end
+    if (last) break;  // linalg.py:437-438: no reciprocal at the end
     __syncthreads();
     // multipliers m_i = mul(A_ij, recip) for local rows i > j
     for (int rr = tid; rr < nr; rr += PANEL_THREADS) {
@@ -253,7 +269,7 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
 #pragma unroll
         for (int c = 0; c < K; ++c) {
           a[c] = at(rr, jj)[c];
-          rc[c] = recip[c];
+          rc[c] = S.recip[c];
         }
         mc::mul<K>(a, rc, o);
 #pragma unroll
@@ -262,7 +278,7 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
     }
     __syncthreads();
     if (jj + 1 >= w) break;
-    // look-ahead: column jj+1 first
+    // look-ahead: column jj+1 first, then publish its candidate
     for (int rr = tid; rr < nr; rr += PANEL_THREADS) {
       if (rbeg + rr > j) {
         double negm[K], u[K], acc[K];
@@ -279,29 +295,25 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
     }
     __syncthreads();
     publish_candidate(jj + 1, seq + 1);
-    // remaining columns (warps 1..) while lane 0 of warp 0 divides
-    if (tid == 0) {
-      spec_div(jj + 1);
-    } else if (tid >= 32) {
-      const int ncol = w - jj - 2;
-      for (int e = tid - 32; e < nr * ncol; e += PANEL_THREADS - 32) {
-        int rr = e / ncol, cc = jj + 2 + e % ncol;
-        if (rbeg + rr > j) {
-          double negm[K], u[K], acc[K];
+    // remaining columns of step jj, then the rows of step jj+1
+    const int ncol = w - jj - 2;
+    for (int e = tid; e < nr * ncol; e += PANEL_THREADS) {
+      int rr = e / ncol, cc = jj + 2 + e % ncol;
+      if (rbeg + rr > j) {
+        double negm[K], u[K], acc[K];
 #pragma unroll
-          for (int c = 0; c < K; ++c) {
-            negm[c] = -at(rr, jj)[c];
-            u[c] = prow[cc * K + c];
-            acc[c] = at(rr, cc)[c];
-          }
-          mc::madd<K>(acc, negm, u);
-#pragma unroll
-          for (int c = 0; c < K; ++c) at(rr, cc)[c] = acc[c];
+        for (int c = 0; c < K; ++c) {
+          negm[c] = -at(rr, jj)[c];
+          u[c] = prow[cc * K + c];
+          acc[c] = at(rr, cc)[c];
         }
+        mc::madd<K>(acc, negm, u);
+#pragma unroll
+        for (int c = 0; c < K; ++c) at(rr, cc)[c] = acc[c];
       }
     }
     __syncthreads();
-    publish_data(jj + 1, seq + 1);
+    publish_rows(jj + 1, seq + 1);
   }
 
   for (int e = tid; e < nr * w; e += PANEL_THREADS) {
@@ -430,7 +442,7 @@ cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block,
 
 template <int K, int W>
 size_t panel_smem(int R) {
-  return ((size_t)R * W * K + W * K + K) * sizeof(double);
+  return ((size_t)R * W * K + W * K) * sizeof(double);
 }
 
 template <int K, int W>
@@ -514,21 +526,17 @@ cudaError_t enqueue_lu(int k, int n, MatView A, int32_t *d_swaps, int nb,
 cudaError_t LuWork::init(int sms) {
   G = sms;
   cudaError_t e;
-  size_t words = (size_t)2 * G * 4 * sizeof(u64);
-  if ((e = cudaMalloc(&cand_words, words)) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&data_seq, 2 * G * sizeof(u64))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&cand_rows, (size_t)2 * G * LU_ROW_STRIDE *
-                                      sizeof(double))) != cudaSuccess)
-    return e;
-  if ((e = cudaMalloc(&rowj, 2 * LU_ROW_STRIDE * sizeof(double))) !=
-      cudaSuccess)
-    return e;
-  if ((e = cudaMalloc(&rowj_seq, 2 * sizeof(u64))) != cudaSuccess) return e;
+  size_t cw = (size_t)2 * G * LU_CAND_WORDS * sizeof(u64);
+  size_t rwb = (size_t)2 * G * LU_ROW_WORDS * sizeof(u64);
+  size_t jw = (size_t)2 * LU_ROW_WORDS * sizeof(u64);
+  if ((e = cudaMalloc(&cand_words, cw)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&row_words, rwb)) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&rowj_words, jw)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&epoch, sizeof(unsigned))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&status, sizeof(int32_t))) != cudaSuccess) return e;
-  cudaMemset(cand_words, 0, words);
-  cudaMemset(data_seq, 0, 2 * G * sizeof(u64));
-  cudaMemset(rowj_seq, 0, 2 * sizeof(u64));
+  cudaMemset(cand_words, 0, cw);
+  cudaMemset(row_words, 0, rwb);
+  cudaMemset(rowj_words, 0, jw);
   cudaMemset(epoch, 0, sizeof(unsigned));
   cudaMemset(status, 0xFF, sizeof(int32_t));
   graphs = new GraphCache();
