@@ -153,6 +153,9 @@ int32_t mpcore_sync(void);
 int32_t mpcore_prof_enable(int32_t on);
 int32_t mpcore_prof_reset(void);
 int32_t mpcore_prof_read(double *ms, int64_t *launches, int32_t cap);
+/* diagnostics: per-CTA, per-column phase timestamps (ns) of the panel
+ * selected by the MPCORE_TRACE_PANEL environment variable; [SMs][32][8] */
+int32_t mpcore_debug_panel_trace(uint64_t *out_ns, int64_t cap);
 /* FP64 issue-rate microbenchmark: DADD instructions per second */
 int32_t mpcore_fp64_peak(double *dadd_per_s, double *dfma_per_s);
 

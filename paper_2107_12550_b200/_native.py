@@ -70,6 +70,7 @@ _PROTOS = {
     "mpcore_prof_reset": (_i32, []),
     "mpcore_prof_read": (_i32, [_dp, ctypes.POINTER(_i64), _i32]),
     "mpcore_fp64_peak": (_i32, [_dp, _dp]),
+    "mpcore_debug_panel_trace": (_i32, [ctypes.POINTER(_u64), _i64]),
 }
 
 # The 16 symbols of the reference ABI (build_lib.py:31-57).

@@ -165,6 +165,13 @@ int ensure_device_locked() {
     D.why = std::string("workspace: ") + cudaGetErrorString(e);
     return fail(MPCORE_INTERNAL, D.why);
   }
+  if (const char *t = std::getenv("MPCORE_TRACE_PANEL")) {
+    size_t bytes = (size_t)D.sms * 32 * 8 * sizeof(unsigned long long);
+    if (cudaMalloc(&D.ws.trace, bytes) == cudaSuccess) {
+      cudaMemset(D.ws.trace, 0, bytes);
+      D.ws.trace_J = std::atoi(t);
+    }
+  }
   D.ok = true;
   return MPCORE_OK;
 }
@@ -873,6 +880,19 @@ int32_t mpcore_prof_reset(void) {
     P.ms[i] = 0;
     P.launches[i] = 0;
   }
+  return MPCORE_OK;
+}
+
+int32_t mpcore_debug_panel_trace(uint64_t *out_ns, int64_t cap) {
+  DevLock L;
+  if (L.st) return L.st;
+  Device &D = device();
+  int64_t count = (int64_t)D.sms * 32 * 8;
+  if (!D.ws.trace) return fail(MPCORE_INTERNAL, "MPCORE_TRACE_PANEL not set");
+  if (!out_ns || cap < count) return MPCORE_BAD_DIMENSION;
+  cudaError_t e = cudaMemcpy(out_ns, D.ws.trace, count * sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "trace");
   return MPCORE_OK;
 }
 

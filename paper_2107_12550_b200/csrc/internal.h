@@ -38,6 +38,8 @@ struct LuWork {
   int32_t *status = nullptr;                 // [0] singular step (or -1)
   int G = 0;                                 // max CTAs of the panel launch
   void *graphs = nullptr;                    // host-side graph cache
+  unsigned long long *trace = nullptr;       // diagnostics: [G][32][8] ns
+  int trace_J = -1;                          // panel to trace (-1: none)
   cudaError_t init(int sms);
 };
 

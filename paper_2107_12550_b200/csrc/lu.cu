@@ -45,15 +45,21 @@ namespace {
 
 constexpr int PANEL_THREADS = 256;
 constexpr int NWARPS = PANEL_THREADS / 32;
+#ifndef POLL_NS
+#define POLL_NS 32
+#endif
 typedef unsigned long long u64;
 
+// GPU-scope relaxed accesses: single-copy atomic 8-byte words, no ordering
+// needed beyond that (every word carries its own sequence number).
+// (.volatile would be system scope.)
 __device__ __forceinline__ void st_volatile(u64 *p, u64 v) {
-  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v)
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v)
                : "memory");
 }
 __device__ __forceinline__ u64 ld_volatile(const u64 *p) {
   u64 v;
-  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p)
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p)
                : "memory");
   return v;
 }
@@ -94,235 +100,7 @@ __device__ __forceinline__ void block_argmax(double &mag, int &row,
   row = s_row[NWARPS];
 }
 
-struct PanelShared {
-  double s_mag[NWARPS + 1];
-  int s_row[NWARPS + 1];
-  double recip[LU_MAX_K];
-  int cand_row;        // local candidate (global row index) of the step
-};
-
-// LL word helpers: a double travels as two words (low half, high half)
-__device__ __forceinline__ unsigned lo32(double v) {
-  return (unsigned)((unsigned long long)__double_as_longlong(v) & 0xffffffffu);
-}
-__device__ __forceinline__ unsigned hi32(double v) {
-  return (unsigned)((unsigned long long)__double_as_longlong(v) >> 32);
-}
-
-template <int K, int W>
-__global__ void __launch_bounds__(PANEL_THREADS, 1)
-panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
-             LuWork ws) {
-  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
-  if (ws.status[0] >= 0) return;
-  // sequence numbers: unique per LU call (device epoch) and column
-  const unsigned seq0 = ws.epoch[0] * 65536u + (unsigned)J + 1u;
-  const int m = n - J;
-  const int R = (m + G - 1) / G;
-  const int rbeg = J + g * R;
-  const int nr = max(0, min(rbeg + R, n) - rbeg);
-  const int rw = 2 * w * K;  // LL words per panel row
-  extern __shared__ double sm[];
-  double *rows = sm;                  // [R][W][K]
-  double *prow = rows + R * W * K;    // [W][K] pivot row of this step
-  __shared__ PanelShared S;
-
-  auto at = [&](int r, int col) -> double * { return rows + (r * W + col) * K; };
-
-  for (int e = tid; e < nr * w; e += PANEL_THREADS) {
-    int r = e / w, col = e % w;
-#pragma unroll
-    for (int c = 0; c < K; ++c)
-      at(r, col)[c] = A.p[c * A.plane + (int64_t)(rbeg + r) * A.ld + J + col];
-  }
-  __syncthreads();
-
-  // (a) local first-max candidate of column jj; words: idx, |head| (2),
-  //     pivot value (2K) -- self-validating, no fence needed
-  auto publish_candidate = [&](int jj, unsigned seq) {
-    const int j = J + jj;
-    double mag = -1.0;
-    int row = INT_MAX;
-    for (int r = tid; r < nr; r += PANEL_THREADS) {
-      int gi = rbeg + r;
-      if (gi >= j) {
-        double v = fabs(at(r, jj)[0]);
-        if (better(v, gi, mag, row)) { mag = v; row = gi; }
-      }
-    }
-    block_argmax(mag, row, S.s_mag, S.s_row);
-    u64 *wd = ws.cand_words + ((int64_t)(jj & 1) * G + g) * LU_CAND_WORDS;
-    if (tid == 0) {
-      S.cand_row = row;
-      st_volatile(wd + 0, ll_word((unsigned)row, seq));
-      st_volatile(wd + 1, ll_word(lo32(mag), seq));
-      st_volatile(wd + 2, ll_word(hi32(mag), seq));
-    } else if (tid <= 2 * K && row != INT_MAX) {
-      const double v = at(row - rbeg, jj)[(tid - 1) >> 1];
-      st_volatile(wd + 2 + tid, ll_word((tid & 1) ? lo32(v) : hi32(v), seq));
-    }
-  };
-  // (b) candidate row and (if owned) row j, once every column is current
-  auto publish_rows = [&](int jj, unsigned seq) {
-    const int j = J + jj, par = jj & 1;
-    const int row = S.cand_row;
-    if (row != INT_MAX) {
-      u64 *wd = ws.row_words + ((int64_t)par * G + g) * LU_ROW_WORDS;
-      const double *src = at(row - rbeg, 0);
-      for (int e = tid; e < rw; e += PANEL_THREADS) {
-        double v = src[e >> 1];
-        st_volatile(wd + e, ll_word((e & 1) ? hi32(v) : lo32(v), seq));
-      }
-    }
-    if (j >= rbeg && j < rbeg + nr) {
-      u64 *wd = ws.rowj_words + (int64_t)par * LU_ROW_WORDS;
-      const double *src = at(j - rbeg, 0);
-      for (int e = tid; e < rw; e += PANEL_THREADS) {
-        double v = src[e >> 1];
-        st_volatile(wd + e, ll_word((e & 1) ? hi32(v) : lo32(v), seq));
-      }
-    }
-  };
-  // poll one LL word until it carries `seq`; return its payload
-  auto poll = [](const u64 *p, unsigned seq) -> unsigned {
-    u64 v;
-    do {
-      v = ld_volatile(p);
-    } while ((unsigned)v != seq);
-    return (unsigned)(v >> 32);
-  };
-
-  publish_candidate(0, seq0);
-  __syncthreads();
-  publish_rows(0, seq0);
-
-  for (int jj = 0; jj < w; ++jj) {
-    const int j = J + jj, par = jj & 1;
-    const unsigned seq = seq0 + jj;
-    // (c) global first max over all candidates: one L2 round trip
-    double gm = -1.0;
-    int gr = INT_MAX;
-    if (tid < G) {
-      const u64 *wd = ws.cand_words + ((int64_t)par * G + tid) * LU_CAND_WORDS;
-      unsigned a = poll(wd + 0, seq);
-      unsigned b = poll(wd + 1, seq);
-      unsigned c = poll(wd + 2, seq);
-      gr = (int)a;
-      gm = __longlong_as_double((long long)(((u64)c << 32) | b));
-    }
-    block_argmax(gm, gr, S.s_mag, S.s_row);
-    const int r = gr;
-    const int gw = (r - J) / R;
-    const bool own_r = r >= rbeg && r < rbeg + nr;
-    const bool own_j = j >= rbeg && j < rbeg + nr;
-    const bool last = (j == n - 1);
-    // warp 0: pivot value -> recip = div(1, pivot) (every CTA, same bits);
-    // other warps: the winner's pivot row (and row j for the new owner of r)
-    if (tid < 32) {
-      if (!last) {
-        const u64 *wd = ws.cand_words + ((int64_t)par * G + gw) * LU_CAND_WORDS;
-        unsigned half = tid < 2 * K ? poll(wd + 3 + tid, seq) : 0u;
-        double pv[K];
-#pragma unroll
-        for (int c = 0; c < K; ++c) {
-          unsigned l = __shfl_sync(0xffffffffu, half, 2 * c);
-          unsigned h = __shfl_sync(0xffffffffu, half, 2 * c + 1);
-          pv[c] = __longlong_as_double((long long)(((u64)h << 32) | l));
-        }
-        if (tid == 0 && pv[0] != 0.0) {
-          double one[K], q[K];
-#pragma unroll
-          for (int c = 0; c < K; ++c) one[c] = c == 0 ? 1.0 : 0.0;
-          mc::div<K>(one, pv, q);
-#pragma unroll
-          for (int c = 0; c < K; ++c) S.recip[c] = q[c];
-        }
-      }
-    } else {
-      const u64 *wd = ws.row_words + ((int64_t)par * G + gw) * LU_ROW_WORDS;
-      unsigned *pr = reinterpret_cast<unsigned *>(prow);
-      for (int e = tid - 32; e < rw; e += PANEL_THREADS - 32)
-        pr[e] = poll(wd + e, seq);
-      if (r != j && own_r) {
-        const u64 *wj = ws.rowj_words + (int64_t)par * LU_ROW_WORDS;
-        unsigned *dst = reinterpret_cast<unsigned *>(at(r - rbeg, 0));
-        for (int e = tid - 32; e < rw; e += PANEL_THREADS - 32)
-          dst[e] = poll(wj + e, seq);
-      }
-    }
-    __syncthreads();
-    if (r != j && own_j) {
-      double *dst = at(j - rbeg, 0);
-      for (int e = tid; e < w * K; e += PANEL_THREADS) dst[e] = prow[e];
-    }
-    if (g == 0 && tid == 0) swaps[j] = r;
-    if (prow[jj * K] == 0.0) {  // singular at step j (uniform decision)
-      if (g == 0 && tid == 0) ws.status[0] = j;
-      return;
-    }
-    if (last) break;  // linalg.py:437-438: no reciprocal at the end
-    __syncthreads();
-    // multipliers m_i = mul(A_ij, recip) for local rows i > j
-    for (int rr = tid; rr < nr; rr += PANEL_THREADS) {
-      if (rbeg + rr > j) {
-        double a[K], rc[K], o[K];
-#pragma unroll
-        for (int c = 0; c < K; ++c) {
-          a[c] = at(rr, jj)[c];
-          rc[c] = S.recip[c];
-        }
-        mc::mul<K>(a, rc, o);
-#pragma unroll
-        for (int c = 0; c < K; ++c) at(rr, jj)[c] = o[c];
-      }
-    }
-    __syncthreads();
-    if (jj + 1 >= w) break;
-    // look-ahead: column jj+1 first, then publish its candidate
-    for (int rr = tid; rr < nr; rr += PANEL_THREADS) {
-      if (rbeg + rr > j) {
-        double negm[K], u[K], acc[K];
-#pragma unroll
-        for (int c = 0; c < K; ++c) {
-          negm[c] = -at(rr, jj)[c];
-          u[c] = prow[(jj + 1) * K + c];
-          acc[c] = at(rr, jj + 1)[c];
-        }
-        mc::madd<K>(acc, negm, u);
-#pragma unroll
-        for (int c = 0; c < K; ++c) at(rr, jj + 1)[c] = acc[c];
-      }
-    }
-    __syncthreads();
-    publish_candidate(jj + 1, seq + 1);
-    // remaining columns of step jj, then the rows of step jj+1
-    const int ncol = w - jj - 2;
-    for (int e = tid; e < nr * ncol; e += PANEL_THREADS) {
-      int rr = e / ncol, cc = jj + 2 + e % ncol;
-      if (rbeg + rr > j) {
-        double negm[K], u[K], acc[K];
-#pragma unroll
-        for (int c = 0; c < K; ++c) {
-          negm[c] = -at(rr, jj)[c];
-          u[c] = prow[cc * K + c];
-          acc[c] = at(rr, cc)[c];
-        }
-        mc::madd<K>(acc, negm, u);
-#pragma unroll
-        for (int c = 0; c < K; ++c) at(rr, cc)[c] = acc[c];
-      }
-    }
-    __syncthreads();
-    publish_rows(jj + 1, seq + 1);
-  }
-
-  for (int e = tid; e < nr * w; e += PANEL_THREADS) {
-    int r = e / w, col = e % w;
-#pragma unroll
-    for (int c = 0; c < K; ++c)
-      A.p[c * A.plane + (int64_t)(rbeg + r) * A.ld + J + col] = at(r, col)[c];
-  }
-}
+#include "panel.cuh"
 
 __global__ void lu_begin_kernel(unsigned *epoch, int32_t *status) {
   epoch[0] += 1u;
@@ -340,21 +118,38 @@ laswp_kernel(MatView A, int J, int w, int c0, int c1, int c2, int c3,
   if (status[0] >= 0) return;
   __shared__ int cur[2 * LU_MAX_W], src[2 * LU_MAX_W];
   __shared__ int cnt;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // warp 0 composes the swaps; lane l holds entries l and l+32
+    const int lane = threadIdx.x;
+    int c0 = -1, s0 = -1, c1 = -1, s1 = -1;  // (row, original source)
     int m = 0;
+    const int mine = lane < w ? swaps[J + lane] : 0;  // one load per lane
     for (int jj = 0; jj < w; ++jj) {
-      int a = J + jj, b = swaps[a];
+      const int a = J + jj, b = __shfl_sync(0xffffffffu, mine, jj);
       if (a == b) continue;
-      int ia = -1, ib = -1;
-      for (int t = 0; t < m; ++t) {
-        if (cur[t] == a) ia = t;
-        if (cur[t] == b) ib = t;
+      unsigned fa = __ballot_sync(0xffffffffu, c0 == a) |
+                    0, fa1 = __ballot_sync(0xffffffffu, c1 == a);
+      unsigned fb = __ballot_sync(0xffffffffu, c0 == b),
+               fb1 = __ballot_sync(0xffffffffu, c1 == b);
+      int ia = fa ? __ffs(fa) - 1 : (fa1 ? 32 + __ffs(fa1) - 1 : -1);
+      int ib = fb ? __ffs(fb) - 1 : (fb1 ? 32 + __ffs(fb1) - 1 : -1);
+      if (ia < 0) {
+        ia = m++;
+        if (lane == (ia & 31)) { if (ia < 32) { c0 = a; s0 = a; } else { c1 = a; s1 = a; } }
       }
-      if (ia < 0) { cur[m] = a; src[m] = a; ia = m++; }
-      if (ib < 0) { cur[m] = b; src[m] = b; ib = m++; }
-      int t = src[ia]; src[ia] = src[ib]; src[ib] = t;
+      if (ib < 0) {
+        ib = m++;
+        if (lane == (ib & 31)) { if (ib < 32) { c0 = b; s0 = b; } else { c1 = b; s1 = b; } }
+      }
+      // exchange the sources of entries ia and ib
+      int sa = __shfl_sync(0xffffffffu, ia < 32 ? s0 : s1, ia & 31);
+      int sb = __shfl_sync(0xffffffffu, ib < 32 ? s0 : s1, ib & 31);
+      if (lane == (ia & 31)) { if (ia < 32) s0 = sb; else s1 = sb; }
+      if (lane == (ib & 31)) { if (ib < 32) s0 = sa; else s1 = sa; }
     }
-    cnt = m;
+    if (lane < m) { cur[lane] = c0; src[lane] = s0; }
+    if (lane + 32 < m) { cur[lane + 32] = c1; src[lane + 32] = s1; }
+    if (lane == 0) cnt = m;
   }
   __syncthreads();
   const int m = cnt;
@@ -449,7 +244,16 @@ template <int K, int W>
 cudaError_t panel_k(int n, MatView A, int J, int w, int32_t *d_swaps,
                     LuWork &ws, cudaStream_t s) {
   const int m = n - J;
-  int G = min(ws.G, max(1, (m + 7) / 8));
+  // Rows per CTA: the per-column candidate exchange costs ~0.6 us among 16
+  // CTAs, ~0.9 us among 64 and ~1.9 us among 148 (tools/llbench.cu on
+  // B200), while warp 0 handles up to 32 rows at the cost of one; so aim
+  // for 32+ rows per CTA rather than spreading over every SM.
+  static const int rows_target = [] {
+    const char *e = std::getenv("MPCORE_PANEL_ROWS");
+    int v = e ? std::atoi(e) : 32;
+    return v > 0 ? v : 32;
+  }();
+  int G = min(ws.G, max(1, (m + rows_target - 1) / rows_target));
   const int R = (m + G - 1) / G;
   size_t smem = panel_smem<K, W>(R);
   auto kern = panel_kernel<K, W>;

@@ -1,0 +1,366 @@
+// Panel factorisation kernel (included by lu.cu; see the protocol notes at
+// the top of lu.cu).  Warp-specialised:
+//   warp 0 ("W0") runs the per-column critical chain with warp-level
+//     synchronisation only: poll every CTA's candidate words, global first
+//     max (redux.sync), recip = div(1, pivot) (all lanes, same bits),
+//     multipliers, look-ahead update of the next column, local first max of
+//     that column, publish the next candidate;
+//   warps 1..7 ("H") stream the winner's pivot row, apply the row exchange,
+//     run the rank-1 update of the remaining panel columns and publish the
+//     candidate rows;
+// coupled by named barriers (bar.arrive by the producer, bar.sync by the
+// consumer, 256 threads per barrier):
+//   B_WIN  W0 -> H : winner of column jj known (smem)
+//   B_ROW  H -> W0 : pivot row staged, swap applied
+//   B_MUL  W0 -> H : multipliers of column jj + next candidate row known
+//   B_REM  H -> W0 : remaining update of column jj done, rows published
+//
+// Included inside namespace mpk::{anonymous} of lu.cu (uses its helpers).
+#pragma once
+
+constexpr int B_WIN = 1, B_ROW = 2, B_MUL = 3, B_REM = 4, B_H = 5;
+constexpr int H_THREADS = PANEL_THREADS - 32;
+
+// a double travels as two LL words (low half, high half)
+__device__ __forceinline__ unsigned lo32(double v) {
+  return (unsigned)((unsigned long long)__double_as_longlong(v) & 0xffffffffu);
+}
+__device__ __forceinline__ unsigned hi32(double v) {
+  return (unsigned)((unsigned long long)__double_as_longlong(v) >> 32);
+}
+
+__device__ __forceinline__ void nb_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void nb_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// warp-wide first max of (mag >= 0 or -1, row): larger |head| first, then
+// the smaller row (np.argmax).  Non-negative doubles order like their bit
+// patterns, so three integer reductions decide it exactly.
+__device__ __forceinline__ void warp_argmax(double mag, int row, double &out_mag,
+                                            int &out_row) {
+  const bool valid = row != INT_MAX && mag >= 0.0;
+  unsigned long long b = valid ? (unsigned long long)__double_as_longlong(mag) : 0ull;
+  unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+  unsigned vmask = __ballot_sync(0xffffffffu, valid);
+  if (!valid) hi = 0u;
+  unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  unsigned lo_c = (valid && hi == mhi) ? lo : 0u;
+  unsigned mlo = __reduce_max_sync(0xffffffffu, lo_c);
+  unsigned rc = (valid && hi == mhi && lo == mlo) ? (unsigned)row : 0xffffffffu;
+  unsigned mrow = __reduce_min_sync(0xffffffffu, rc);
+  if (vmask == 0u) {
+    out_mag = -1.0;
+    out_row = INT_MAX;
+  } else {
+    out_row = (int)mrow;
+    out_mag = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+  }
+}
+
+struct PanelSmem {
+  double recip[LU_MAX_K];
+  int winner;      // global row of the pivot of the current column
+  int gw;          // CTA owning it
+  int cand_row;    // this CTA's candidate for the next column
+  int flag;        // 1 singular / last column: stop after B_WIN
+  int singular;    // 1: stop without write-back
+};
+
+template <int K, int W>
+__global__ void __launch_bounds__(PANEL_THREADS, 1)
+panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
+             LuWork ws) {
+  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31;
+  if (ws.status[0] >= 0) return;
+  const unsigned seq0 = ws.epoch[0] * 65536u + (unsigned)J + 1u;
+  const int m = n - J;
+  const int R = (m + G - 1) / G;
+  const int rbeg = J + g * R;
+  const int nr = max(0, min(rbeg + R, n) - rbeg);
+  const int rw = 2 * w * K;
+  extern __shared__ double sm[];
+  double *rows = sm;                  // [R][W][K]
+  double *prow = rows + R * W * K;    // [W][K]
+  __shared__ PanelSmem S;
+  auto at = [&](int r, int col) -> double * { return rows + (r * W + col) * K; };
+
+  for (int e = tid; e < nr * w; e += PANEL_THREADS) {
+    int r = e / w, col = e % w;
+#pragma unroll
+    for (int c = 0; c < K; ++c)
+      at(r, col)[c] = A.p[c * A.plane + (int64_t)(rbeg + r) * A.ld + J + col];
+  }
+  if (tid == 0) {
+    S.flag = 0;
+    S.singular = 0;
+  }
+  __syncthreads();
+
+  // W0: local first max of column jj (rows >= J+jj) and its candidate words
+  auto w0_publish_candidate = [&](int jj, unsigned seq) {
+    const int j = J + jj;
+    double mag = -1.0;
+    int row = INT_MAX;
+    for (int r = lane; r < nr; r += 32) {
+      int gi = rbeg + r;
+      if (gi >= j) {
+        double v = fabs(at(r, jj)[0]);
+        if (better(v, gi, mag, row)) { mag = v; row = gi; }
+      }
+    }
+    double bm;
+    int br;
+    warp_argmax(mag, row, bm, br);
+    u64 *wd = ws.cand_words + ((int64_t)(jj & 1) * G + g) * LU_CAND_WORDS;
+    if (lane == 0) {
+      S.cand_row = br;
+      st_volatile(wd + 0, ll_word((unsigned)br, seq));
+      st_volatile(wd + 1, ll_word(lo32(bm), seq));
+      st_volatile(wd + 2, ll_word(hi32(bm), seq));
+    } else if (lane <= 2 * K && br != INT_MAX) {
+      const double v = at(br - rbeg, jj)[(lane - 1) >> 1];
+      st_volatile(wd + 2 + lane, ll_word((lane & 1) ? lo32(v) : hi32(v), seq));
+    }
+  };
+  // H: publish the candidate row of column jj (+ row J+jj if owned)
+  auto h_publish_rows = [&](int jj, unsigned seq, int row) {
+    const int j = J + jj, par = jj & 1, ht = tid - 32;
+    if (row != INT_MAX) {
+      u64 *wd = ws.row_words + ((int64_t)par * G + g) * LU_ROW_WORDS;
+      const double *src = at(row - rbeg, 0);
+      for (int e = ht; e < rw; e += H_THREADS) {
+        double v = src[e >> 1];
+        st_volatile(wd + e, ll_word((e & 1) ? hi32(v) : lo32(v), seq));
+      }
+    }
+    if (j >= rbeg && j < rbeg + nr) {
+      u64 *wd = ws.rowj_words + (int64_t)par * LU_ROW_WORDS;
+      const double *src = at(j - rbeg, 0);
+      for (int e = ht; e < rw; e += H_THREADS) {
+        double v = src[e >> 1];
+        st_volatile(wd + e, ll_word((e & 1) ? hi32(v) : lo32(v), seq));
+      }
+    }
+  };
+  const bool tracing = ws.trace != nullptr && ws.trace_J == J && tid == 0;
+  auto trace = [&](int jj, int slot) {
+    if (tracing) {
+      unsigned long long t;
+      if (slot == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        ws.trace[((int64_t)g * 32 + jj) * 8 + 7] = t;
+      }
+      t = clock64();
+      ws.trace[((int64_t)g * 32 + jj) * 8 + slot] = t;
+    }
+  };
+  auto poll = [](const u64 *p, unsigned seq) -> unsigned {
+    u64 v = ld_volatile(p);
+    while ((unsigned)v != seq) {
+      __nanosleep(POLL_NS);
+      v = ld_volatile(p);
+    }
+    return (unsigned)(v >> 32);
+  };
+
+  // prologue: candidate and rows of column 0 (all columns current)
+  if (tid < 32) w0_publish_candidate(0, seq0);
+  __syncthreads();
+  if (tid >= 32) h_publish_rows(0, seq0, S.cand_row);
+
+  if (tid < 32) {
+    // ================================================================ W0 ==
+    for (int jj = 0; jj < w; ++jj) {
+      const int j = J + jj, par = jj & 1;
+      const unsigned seq = seq0 + jj;
+      trace(jj, 0);
+      // one round trip: every slot's index, |head| and pivot value
+      constexpr int SPL = 5;        // slots per lane (G <= 160)
+      constexpr int NW = 3 + 2 * K; // words per slot
+      u64 wv[SPL][NW];
+      unsigned done = 0;  // bit q: slot lane+32q complete (or absent)
+#pragma unroll
+      for (int q = 0; q < SPL; ++q)
+        if (lane + 32 * q >= G) done |= 1u << q;
+      for (;;) {
+#pragma unroll
+        for (int q = 0; q < SPL; ++q) {
+          if (!(done & (1u << q))) {
+            const u64 *wd = ws.cand_words +
+                            ((int64_t)par * G + lane + 32 * q) * LU_CAND_WORDS;
+#pragma unroll
+            for (int x = 0; x < NW; ++x) wv[q][x] = ld_volatile(wd + x);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < SPL; ++q) {
+          if (!(done & (1u << q))) {
+            bool head = true, piv = true;
+#pragma unroll
+            for (int x = 0; x < 3; ++x)
+              if ((unsigned)wv[q][x] != seq) head = false;
+#pragma unroll
+            for (int x = 3; x < NW; ++x)
+              if ((unsigned)wv[q][x] != seq) piv = false;
+            // a CTA without rows >= j publishes no pivot value
+            if (head && ((int)(wv[q][0] >> 32) == INT_MAX || piv))
+              done |= 1u << q;
+          }
+        }
+        if (__all_sync(0xffffffffu, done == (1u << SPL) - 1u)) break;
+        __nanosleep(POLL_NS);
+      }
+      double bm = -1.0;
+      int br = INT_MAX;
+#pragma unroll
+      for (int q = 0; q < SPL; ++q) {
+        if (lane + 32 * q < G) {
+          int rr = (int)(wv[q][0] >> 32);
+          double mm = __longlong_as_double(
+              (long long)((wv[q][2] & 0xffffffff00000000ull) | (wv[q][1] >> 32)));
+          if (better(mm, rr, bm, br)) { bm = mm; br = rr; }
+        }
+      }
+      double gm;
+      int r;
+      warp_argmax(bm, br, gm, r);
+      trace(jj, 1);
+      const int gw = (r - J) / R;
+      if (g == 0 && lane == 0) swaps[j] = r;
+      // pivot value of the winner: already in lane gw%32, slot gw/32
+      const int wq = gw >> 5, wl = gw & 31;
+      double pv[K];
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        u64 lw = 0, hw = 0;
+#pragma unroll
+        for (int q = 0; q < SPL; ++q)
+          if (q == wq) {
+            lw = wv[q][3 + 2 * c];
+            hw = wv[q][4 + 2 * c];
+          }
+        unsigned l = __shfl_sync(0xffffffffu, (unsigned)(lw >> 32), wl);
+        unsigned h = __shfl_sync(0xffffffffu, (unsigned)(hw >> 32), wl);
+        pv[c] = __longlong_as_double((long long)(((u64)h << 32) | l));
+      }
+      const bool singular = pv[0] == 0.0;
+      const bool last = (j == n - 1);
+      if (lane == 0) {
+        S.winner = r;
+        S.gw = gw;
+        S.flag = (singular || last) ? 1 : 0;
+        S.singular = singular ? 1 : 0;
+        if (singular && g == 0) ws.status[0] = j;
+      }
+      __syncwarp();
+      nb_arrive(B_WIN, PANEL_THREADS);
+      if (singular) return;
+      if (last) break;
+      // recip = div(1, pivot): every lane computes the same value
+      double one[K], rc[K];
+#pragma unroll
+      for (int c = 0; c < K; ++c) one[c] = c == 0 ? 1.0 : 0.0;
+      mc::div<K>(one, pv, rc);
+      trace(jj, 2);
+      nb_sync(B_ROW, PANEL_THREADS);  // pivot row staged, swap applied
+      trace(jj, 3);
+      // multipliers m_i = mul(A_ij, recip), rows i > j
+      for (int rr = lane; rr < nr; rr += 32) {
+        if (rbeg + rr > j) {
+          double a[K], o[K];
+#pragma unroll
+          for (int c = 0; c < K; ++c) a[c] = at(rr, jj)[c];
+          mc::mul<K>(a, rc, o);
+#pragma unroll
+          for (int c = 0; c < K; ++c) at(rr, jj)[c] = o[c];
+        }
+      }
+      trace(jj, 4);
+      if (jj >= 1) nb_sync(B_REM, PANEL_THREADS);  // H done with column jj-1
+      trace(jj, 5);
+      if (jj + 1 < w) {
+        // look-ahead: column jj+1, then publish its candidate
+        for (int rr = lane; rr < nr; rr += 32) {
+          if (rbeg + rr > j) {
+            double negm[K], u[K], acc[K];
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+              negm[c] = -at(rr, jj)[c];
+              u[c] = prow[(jj + 1) * K + c];
+              acc[c] = at(rr, jj + 1)[c];
+            }
+            mc::madd<K>(acc, negm, u);
+#pragma unroll
+            for (int c = 0; c < K; ++c) at(rr, jj + 1)[c] = acc[c];
+          }
+        }
+        __syncwarp();
+        w0_publish_candidate(jj + 1, seq + 1);
+        trace(jj, 6);
+      }
+      __syncwarp();
+      nb_arrive(B_MUL, PANEL_THREADS);
+      if (jj + 1 >= w) break;
+    }
+  } else {
+    // ================================================================= H ==
+    const int ht = tid - 32;
+    unsigned *pr = reinterpret_cast<unsigned *>(prow);
+    for (int jj = 0; jj < w; ++jj) {
+      const int j = J + jj, par = jj & 1;
+      const unsigned seq = seq0 + jj;
+      nb_sync(B_WIN, PANEL_THREADS);
+      if (S.flag) break;  // singular (W0 has returned) or last column
+      const int r = S.winner, gw = S.gw;
+      const bool own_r = r >= rbeg && r < rbeg + nr;
+      const bool own_j = j >= rbeg && j < rbeg + nr;
+      const u64 *wd = ws.row_words + ((int64_t)par * G + gw) * LU_ROW_WORDS;
+      for (int e = ht; e < rw; e += H_THREADS) pr[e] = poll(wd + e, seq);
+      if (r != j && own_r) {
+        const u64 *wj = ws.rowj_words + (int64_t)par * LU_ROW_WORDS;
+        unsigned *dst = reinterpret_cast<unsigned *>(at(r - rbeg, 0));
+        for (int e = ht; e < rw; e += H_THREADS) dst[e] = poll(wj + e, seq);
+      }
+      nb_sync(B_H, H_THREADS);
+      if (r != j && own_j) {
+        double *dst = at(j - rbeg, 0);
+        for (int e = ht; e < w * K; e += H_THREADS) dst[e] = prow[e];
+      }
+      nb_sync(B_H, H_THREADS);
+      nb_arrive(B_ROW, PANEL_THREADS);
+      nb_sync(B_MUL, PANEL_THREADS);   // multipliers + next candidate known
+      if (jj + 1 >= w) break;
+      const int ncol = w - jj - 2;
+      for (int e = ht; e < nr * ncol; e += H_THREADS) {
+        int rr = e / ncol, cc = jj + 2 + e % ncol;
+        if (rbeg + rr > j) {
+          double negm[K], u[K], acc[K];
+#pragma unroll
+          for (int c = 0; c < K; ++c) {
+            negm[c] = -at(rr, jj)[c];
+            u[c] = prow[cc * K + c];
+            acc[c] = at(rr, cc)[c];
+          }
+          mc::madd<K>(acc, negm, u);
+#pragma unroll
+          for (int c = 0; c < K; ++c) at(rr, cc)[c] = acc[c];
+        }
+      }
+      nb_sync(B_H, H_THREADS);
+      h_publish_rows(jj + 1, seq + 1, S.cand_row);
+      nb_arrive(B_REM, PANEL_THREADS);
+    }
+  }
+  if (S.singular) return;  // uniform across the grid: no write-back
+  __syncthreads();
+  for (int e = tid; e < nr * w; e += PANEL_THREADS) {
+    int r = e / w, col = e % w;
+#pragma unroll
+    for (int c = 0; c < K; ++c)
+      A.p[c * A.plane + (int64_t)(rbeg + r) * A.ld + J + col] = at(r, col)[c];
+  }
+}

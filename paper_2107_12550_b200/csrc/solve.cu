@@ -9,12 +9,13 @@
 // descending j backward).
 //
 // Parallel structure: rows are cut into blocks of RB; one CTA thread owns
-// one row and runs its chain in registers.  A block consumes the columns of
-// every earlier block as soon as that block has published its final x
-// values (flag per block, epoch-tagged), staging L/U tiles through shared
-// memory with coalesced loads, then resolves its own diagonal triangle and
-// publishes.  CTAs are persistent (cooperative launch => co-resident) and
-// take blocks in dependency order, so the wavefront pipelines across SMs.
+// one row and runs its chain in registers.  Columns are consumed in tiles of
+// CB: a tile of x becomes readable as soon as the CB rows it covers are
+// final (per-tile flag, epoch-tagged), so the next block starts on a tile
+// while the producing block is still resolving later rows of its diagonal
+// triangle.  L/U tiles are staged through shared memory with coalesced,
+// double-buffered cp.async loads.  CTAs are persistent (cooperative launch
+// => co-resident) and take blocks in dependency order.
 #include "internal.h"
 #include "mc.cuh"
 
@@ -23,26 +24,39 @@ namespace mpk {
 namespace {
 
 constexpr int RB = 128;  // rows per block (= threads per CTA)
-constexpr int CB = 16;   // columns per staged tile
+constexpr int CB = 16;   // columns per staged tile (= rows per flag)
 
-__device__ __forceinline__ void wait_flag(const int *flags, int blk,
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s),
+               "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() {
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+template <int N> __device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void wait_flag(const int *flags, int t,
                                           int epoch) {
   if (threadIdx.x == 0) {
-    const volatile int *f = flags + blk;
-    while (*f < epoch) {
-    }
+    const volatile int *f = flags + t;
+    while (*f < epoch) __nanosleep(20);
     __threadfence();
   }
   __syncthreads();
 }
 
-__device__ __forceinline__ void publish_flag(int *flags, int blk, int epoch) {
+// the x rows of tile t are final: make them visible, then raise its flag
+__device__ __forceinline__ void publish(int *flags, int t, int epoch) {
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) atomicExch(flags + blk, epoch);
+  if (threadIdx.x == 0) atomicExch(flags + t, epoch);
 }
 
-// Stage rows [r0, r0+RB) x cols [c0, c0+cw) of M into Ts[c][r][CB+1].
+// Stage rows [r0, r0+RB) x cols [c0, c0+cw) of M into Ts[c][r][CB+1]
+// (asynchronous; caller commits / waits)
 template <int K>
 __device__ __forceinline__ void stage_tile(double *Ts, MatView M, int n,
                                            int r0, int c0, int cw) {
@@ -51,8 +65,8 @@ __device__ __forceinline__ void stage_tile(double *Ts, MatView M, int n,
     if (r0 + r < n && cc < cw) {
 #pragma unroll
       for (int c = 0; c < K; ++c)
-        Ts[(c * RB + r) * (CB + 1) + cc] =
-            M.p[c * M.plane + (int64_t)(r0 + r) * M.ld + c0 + cc];
+        cp_async8(Ts + (c * RB + r) * (CB + 1) + cc,
+                  M.p + c * M.plane + (int64_t)(r0 + r) * M.ld + c0 + cc);
     }
   }
 }
@@ -78,32 +92,41 @@ __global__ void permute_kernel(int n, const int32_t *__restrict__ perm,
   for (int c = 0; c < K; ++c) xw[(int64_t)c * n + i] = b[(int64_t)c * n + src];
 }
 
+constexpr int TILE_ELEMS = RB * (CB + 1);
+
 template <int K>
 __global__ void __launch_bounds__(RB)
 forward_kernel(int n, MatView LU, double *__restrict__ x, int *flags,
                int epoch) {
   extern __shared__ double sm[];
-  double *Ls = sm;                          // [K][RB][CB+1]
-  double *xs = Ls + K * RB * (CB + 1);      // [K][CB]
-  double *xown = xs + K * CB;               // [K][RB]
+  double *Ls0 = sm;                          // [2][K][RB][CB+1]
+  double *xs = Ls0 + 2 * K * TILE_ELEMS;     // [K][CB]
+  double *xown = xs + K * CB;                // [K][RB]
   const int nblk = (n + RB - 1) / RB;
   const int tid = threadIdx.x;
   for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const int r0 = blk * RB, i = r0 + tid;
     const bool live = i < n;
+    const int rend = min(n, r0 + RB);
     double acc[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) acc[c] = live ? x[(int64_t)c * n + i] : 0.0;
-    // columns of earlier blocks, ascending
-    int waited = -1;
-    for (int c0 = 0; c0 < r0; c0 += CB) {
-      const int cb = c0 / RB;
-      if (cb != waited) {
-        wait_flag(flags, cb, epoch);
-        waited = cb;
+    // off-diagonal tiles, ascending; L tiles prefetched one ahead
+    const int ntile = r0 / CB;
+    if (ntile > 0) {
+      stage_tile<K>(Ls0, LU, n, r0, 0, CB);
+      cp_commit();
+    }
+    for (int t = 0; t < ntile; ++t) {
+      double *Ls = Ls0 + (t & 1) * K * TILE_ELEMS;
+      if (t + 1 < ntile) {
+        stage_tile<K>(Ls0 + ((t + 1) & 1) * K * TILE_ELEMS, LU, n, r0,
+                      (t + 1) * CB, CB);
+        cp_commit();
       }
-      stage_tile<K>(Ls, LU, n, r0, c0, CB);
-      stage_x<K>(xs, x, n, c0, CB);
+      wait_flag(flags, t, epoch);
+      stage_x<K>(xs, x, n, t * CB, CB);
+      if (t + 1 < ntile) cp_wait<1>(); else cp_wait<0>();
       __syncthreads();
       if (live) {
 #pragma unroll 1
@@ -119,36 +142,35 @@ forward_kernel(int n, MatView LU, double *__restrict__ x, int *flags,
       }
       __syncthreads();
     }
-    // own triangle: columns r0 .. min(n, r0+RB)-2
-    const int rend = min(n, r0 + RB);
-    for (int c0 = r0; c0 < rend - 1; c0 += CB) {
-      const int cw = min(CB, rend - 1 - c0);
-      stage_tile<K>(Ls, LU, n, r0, c0, cw);
+    // diagonal triangle, tile by tile; each finished tile is published
+    for (int c0 = r0; c0 < rend; c0 += CB) {
+      const int cw = min(CB, rend - c0);
+      stage_tile<K>(Ls0, LU, n, r0, c0, cw);
+      cp_commit();
+      cp_wait<0>();
       __syncthreads();
       for (int jj = 0; jj < cw; ++jj) {
         const int j = c0 + jj;
         if (i == j) {
 #pragma unroll
-          for (int c = 0; c < K; ++c) xown[c * RB + tid] = acc[c];
+          for (int c = 0; c < K; ++c) {
+            xown[c * RB + tid] = acc[c];
+            x[(int64_t)c * n + i] = acc[c];   // final
+          }
         }
         __syncthreads();
         if (live && i > j) {
           double l[K], xj[K];
 #pragma unroll
           for (int c = 0; c < K; ++c) {
-            l[c] = -Ls[(c * RB + tid) * (CB + 1) + jj];
+            l[c] = -Ls0[(c * RB + tid) * (CB + 1) + jj];
             xj[c] = xown[c * RB + (j - r0)];
           }
           mc::madd<K>(acc, l, xj);
         }
       }
-      __syncthreads();
+      publish(flags, c0 / CB, epoch);
     }
-    if (live) {
-#pragma unroll
-      for (int c = 0; c < K; ++c) x[(int64_t)c * n + i] = acc[c];
-    }
-    publish_flag(flags, blk, epoch);
   }
 }
 
@@ -157,10 +179,11 @@ __global__ void __launch_bounds__(RB)
 backward_kernel(int n, MatView LU, double *__restrict__ x, int *flags,
                 int epoch) {
   extern __shared__ double sm[];
-  double *Us = sm;
-  double *xs = Us + K * RB * (CB + 1);
-  double *xown = xs + K * CB;               // [K][RB]: -x_j of own block
+  double *Us0 = sm;
+  double *xs = Us0 + 2 * K * TILE_ELEMS;
+  double *xown = xs + K * CB;                // [K][RB]: -x_j of own block
   const int nblk = (n + RB - 1) / RB;
+  const int ntile_all = (n + CB - 1) / CB;
   const int tid = threadIdx.x;
   for (int q = blockIdx.x; q < nblk; q += gridDim.x) {
     const int blk = nblk - 1 - q;
@@ -170,21 +193,28 @@ backward_kernel(int n, MatView LU, double *__restrict__ x, int *flags,
     double acc[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) acc[c] = live ? x[(int64_t)c * n + i] : 0.0;
-    // columns of later blocks, descending: tiles [c0, c0+cw) from the right
-    int waited = -1;
-    for (int cend = n; cend > rend; cend -= CB) {
-      const int c0 = max(rend, cend - CB), cw = cend - c0;
-      const int cb = (cend - 1) / RB;
-      // a tile never straddles blocks: block edges are multiples of RB and
-      // tiles are cut back from n; wait on every block the tile touches
-      for (int b = c0 / RB; b <= cb; ++b) {
-        if (b != waited) {
-          wait_flag(flags, b, epoch);
-          waited = b;
-        }
+    // off-diagonal tiles of later rows, descending (tile index from the top
+    // tile of the matrix down to the first tile after this block)
+    const int t_lo = (rend + CB - 1) / CB;     // first tile after the block
+    const int nt = ntile_all - t_lo;
+    auto tile_c0 = [&](int q2) { return (ntile_all - 1 - q2) * CB; };
+    if (nt > 0) {
+      int c0 = tile_c0(0);
+      stage_tile<K>(Us0, LU, n, r0, c0, min(CB, n - c0));
+      cp_commit();
+    }
+    for (int q2 = 0; q2 < nt; ++q2) {
+      const int c0 = tile_c0(q2), cw = min(CB, n - c0);
+      double *Us = Us0 + (q2 & 1) * K * TILE_ELEMS;
+      if (q2 + 1 < nt) {
+        int c1 = tile_c0(q2 + 1);
+        stage_tile<K>(Us0 + ((q2 + 1) & 1) * K * TILE_ELEMS, LU, n, r0, c1,
+                      min(CB, n - c1));
+        cp_commit();
       }
-      stage_tile<K>(Us, LU, n, r0, c0, cw);
+      wait_flag(flags, c0 / CB, epoch);
       stage_x<K>(xs, x, n, c0, cw);
+      if (q2 + 1 < nt) cp_wait<1>(); else cp_wait<0>();
       __syncthreads();
       if (live) {
 #pragma unroll 1
@@ -200,22 +230,26 @@ backward_kernel(int n, MatView LU, double *__restrict__ x, int *flags,
       }
       __syncthreads();
     }
-    // own triangle, j descending from rend-1 to r0
-    for (int cend = rend; cend > r0; cend -= CB) {
-      const int c0 = max(r0, cend - CB), cw = cend - c0;
-      stage_tile<K>(Us, LU, n, r0, c0, cw);
+    // diagonal triangle, tiles from the bottom; j descending
+    const int last_tile = (rend - 1) / CB;
+    for (int tt = last_tile; tt >= r0 / CB; --tt) {
+      const int c0 = tt * CB, cw = min(CB, rend - c0);
+      stage_tile<K>(Us0, LU, n, r0, c0, cw);
+      cp_commit();
+      cp_wait<0>();
       __syncthreads();
       for (int jj = cw - 1; jj >= 0; --jj) {
         const int j = c0 + jj;
         if (i == j) {
           double u[K], qv[K];
 #pragma unroll
-          for (int c = 0; c < K; ++c) u[c] = Us[(c * RB + tid) * (CB + 1) + jj];
+          for (int c = 0; c < K; ++c) u[c] = Us0[(c * RB + tid) * (CB + 1) + jj];
           mc::div<K>(acc, u, qv);
 #pragma unroll
           for (int c = 0; c < K; ++c) {
             acc[c] = qv[c];
             xown[c * RB + tid] = -qv[c];
+            x[(int64_t)c * n + i] = qv[c];    // final
           }
         }
         __syncthreads();
@@ -223,25 +257,20 @@ backward_kernel(int n, MatView LU, double *__restrict__ x, int *flags,
           double u[K], nx[K];
 #pragma unroll
           for (int c = 0; c < K; ++c) {
-            u[c] = Us[(c * RB + tid) * (CB + 1) + jj];
+            u[c] = Us0[(c * RB + tid) * (CB + 1) + jj];
             nx[c] = xown[c * RB + (j - r0)];
           }
           mc::madd<K>(acc, u, nx);
         }
       }
-      __syncthreads();
+      publish(flags, tt, epoch);
     }
-    if (live) {
-#pragma unroll
-      for (int c = 0; c < K; ++c) x[(int64_t)c * n + i] = acc[c];
-    }
-    publish_flag(flags, blk, epoch);
   }
 }
 
 template <int K>
 size_t solve_smem() {
-  return ((size_t)K * RB * (CB + 1) + K * CB + K * RB) * sizeof(double);
+  return ((size_t)2 * K * TILE_ELEMS + K * CB + K * RB) * sizeof(double);
 }
 
 template <typename F>
@@ -253,52 +282,69 @@ int coop_grid(F kern, size_t smem, int want) {
   return want < cap ? want : cap;
 }
 
+template <typename... KArgs, typename... Args>
+cudaError_t launch_coop(void (*kern)(KArgs...), int grid, size_t smem,
+                        cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(RB);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int K>
 cudaError_t solve_k(int n, MatView LU, const int32_t *perm, const double *b,
                     double *x, SolveWork &sw, cudaStream_t s) {
   const size_t smem = solve_smem<K>();
   auto fk = forward_kernel<K>;
   auto bk = backward_kernel<K>;
+  static bool configured = false;
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem)) != cudaSuccess)
-    return e;
-  if ((e = cudaFuncSetAttribute(bk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem)) != cudaSuccess)
-    return e;
+  if (!configured) {
+    if ((e = cudaFuncSetAttribute(
+             fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+      return e;
+    if ((e = cudaFuncSetAttribute(
+             bk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+      return e;
+    configured = true;
+  }
   const int nblk = (n + RB - 1) / RB;
-  if ((e = sw.ensure(nblk)) != cudaSuccess) return e;
+  const int ntile = (n + CB - 1) / CB;
+  if ((e = sw.ensure(ntile)) != cudaSuccess) return e;
   permute_kernel<K><<<(n + 255) / 256, 256, 0, s>>>(n, perm, b, x);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   int epoch = sw.next_epoch();
-  int G = coop_grid(fk, smem, nblk);
   int *flags = sw.flags;
-  void *fargs[] = {(void *)&n, (void *)&LU, (void *)&x, (void *)&flags,
-                   (void *)&epoch};
-  e = cudaLaunchCooperativeKernel((const void *)fk, dim3(G), dim3(RB), fargs,
-                                  smem, s);
+  e = launch_coop(fk, coop_grid(fk, smem, nblk), smem, s, n, LU, x, flags,
+                  epoch);
   if (e != cudaSuccess) return e;
   int epoch2 = sw.next_epoch();
-  G = coop_grid(bk, smem, nblk);
-  void *bargs[] = {(void *)&n, (void *)&LU, (void *)&x, (void *)&flags,
-                   (void *)&epoch2};
-  return cudaLaunchCooperativeKernel((const void *)bk, dim3(G), dim3(RB),
-                                     bargs, smem, s);
+  return launch_coop(bk, coop_grid(bk, smem, nblk), smem, s, n, LU, x, flags,
+                     epoch2);
 }
 
 }  // namespace
 
-cudaError_t SolveWork::ensure(int nblk) {
-  if (nblk <= cap) return cudaSuccess;
+cudaError_t SolveWork::ensure(int nflags) {
+  if (nflags <= cap) return cudaSuccess;
   if (flags) cudaFree(flags);
   flags = nullptr;
   cap = 0;
   epoch = 0;
-  cudaError_t e = cudaMalloc(&flags, (size_t)nblk * sizeof(int));
+  cudaError_t e = cudaMalloc(&flags, (size_t)nflags * sizeof(int));
   if (e != cudaSuccess) return e;
-  e = cudaMemset(flags, 0, (size_t)nblk * sizeof(int));
+  e = cudaMemset(flags, 0, (size_t)nflags * sizeof(int));
   if (e != cudaSuccess) return e;
-  cap = nblk;
+  cap = nflags;
   return cudaSuccess;
 }
 
