@@ -36,6 +36,7 @@ struct LuWork {
   unsigned long long *rowj_words = nullptr;  // [2][LU_ROW_WORDS]
   unsigned *epoch = nullptr;                 // [1] device LU call counter
   int32_t *status = nullptr;                 // [0] singular step (or -1)
+  int32_t *swap_list = nullptr;              // [64 cur][64 src][count]
   int G = 0;                                 // max CTAs of the panel launch
   void *graphs = nullptr;                    // host-side graph cache
   unsigned long long *trace = nullptr;       // diagnostics: [G][32][8] ns
@@ -85,9 +86,10 @@ cudaError_t lu_solve(int k, int n, MatView LU, const int32_t *d_perm,
 cudaError_t lu_begin(LuWork &ws, cudaStream_t s);
 cudaError_t lu_panel(int k, int n, MatView A, int J, int w, int32_t *d_swaps,
                      LuWork &ws, cudaStream_t s);
-// row exchanges of panel [J, J+w) on columns [c0, c1) and [c2, c3)
-cudaError_t lu_laswp(int k, MatView A, int J, int w, int c0, int c1, int c2,
-                     int c3, const int32_t *d_swaps, const int32_t *status,
+// row exchanges of the last factored panel (composed in ws.swap_list by the
+// panel kernel) on columns [c0, c1) and [c2, c3)
+cudaError_t lu_laswp(int k, MatView A, int c0, int c1, int c2, int c3,
+                     const int32_t *swap_list, const int32_t *status,
                      cudaStream_t s);
 cudaError_t lu_trsm(int k, MatView L11, MatView U12, int w, int ncols,
                     const int32_t *status, cudaStream_t s);

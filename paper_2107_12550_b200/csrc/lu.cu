@@ -107,50 +107,23 @@ __global__ void lu_begin_kernel(unsigned *epoch, int32_t *status) {
   status[0] = -1;
 }
 
-// Row exchanges of panel [J, J+w), composed once per CTA in shared memory:
-// after the swaps, row cur[i] holds what row src[i] held before.  Each
-// thread then moves one column (of one plane): all loads, then all stores.
+// Row exchanges of panel [J, J+w) on every column outside the panel, using
+// the composition the panel kernel left in ws.swap_list (after the swaps,
+// row cur[i] holds what row src[i] held before).  One thread per (column,
+// plane): all loads, then all stores.
 template <int K>
-__global__ void __launch_bounds__(256)
-laswp_kernel(MatView A, int J, int w, int c0, int c1, int c2, int c3,
-             const int32_t *__restrict__ swaps,
+__global__ void __launch_bounds__(128)
+laswp_kernel(MatView A, int c0, int c1, int c2, int c3,
+             const int32_t *__restrict__ swap_list,
              const int32_t *__restrict__ status) {
   if (status[0] >= 0) return;
   __shared__ int cur[2 * LU_MAX_W], src[2 * LU_MAX_W];
   __shared__ int cnt;
-  if (threadIdx.x < 32) {
-    // warp 0 composes the swaps; lane l holds entries l and l+32
-    const int lane = threadIdx.x;
-    int c0 = -1, s0 = -1, c1 = -1, s1 = -1;  // (row, original source)
-    int m = 0;
-    const int mine = lane < w ? swaps[J + lane] : 0;  // one load per lane
-    for (int jj = 0; jj < w; ++jj) {
-      const int a = J + jj, b = __shfl_sync(0xffffffffu, mine, jj);
-      if (a == b) continue;
-      unsigned fa = __ballot_sync(0xffffffffu, c0 == a) |
-                    0, fa1 = __ballot_sync(0xffffffffu, c1 == a);
-      unsigned fb = __ballot_sync(0xffffffffu, c0 == b),
-               fb1 = __ballot_sync(0xffffffffu, c1 == b);
-      int ia = fa ? __ffs(fa) - 1 : (fa1 ? 32 + __ffs(fa1) - 1 : -1);
-      int ib = fb ? __ffs(fb) - 1 : (fb1 ? 32 + __ffs(fb1) - 1 : -1);
-      if (ia < 0) {
-        ia = m++;
-        if (lane == (ia & 31)) { if (ia < 32) { c0 = a; s0 = a; } else { c1 = a; s1 = a; } }
-      }
-      if (ib < 0) {
-        ib = m++;
-        if (lane == (ib & 31)) { if (ib < 32) { c0 = b; s0 = b; } else { c1 = b; s1 = b; } }
-      }
-      // exchange the sources of entries ia and ib
-      int sa = __shfl_sync(0xffffffffu, ia < 32 ? s0 : s1, ia & 31);
-      int sb = __shfl_sync(0xffffffffu, ib < 32 ? s0 : s1, ib & 31);
-      if (lane == (ia & 31)) { if (ia < 32) s0 = sb; else s1 = sb; }
-      if (lane == (ib & 31)) { if (ib < 32) s0 = sa; else s1 = sa; }
-    }
-    if (lane < m) { cur[lane] = c0; src[lane] = s0; }
-    if (lane + 32 < m) { cur[lane + 32] = c1; src[lane + 32] = s1; }
-    if (lane == 0) cnt = m;
+  if (threadIdx.x < 2 * LU_MAX_W) {
+    cur[threadIdx.x] = swap_list[threadIdx.x];
+    src[threadIdx.x] = swap_list[2 * LU_MAX_W + threadIdx.x];
   }
+  if (threadIdx.x == 0) cnt = swap_list[4 * LU_MAX_W];
   __syncthreads();
   const int m = cnt;
   if (m == 0) return;
@@ -309,7 +282,7 @@ cudaError_t enqueue_lu(int k, int n, MatView A, int32_t *d_swaps, int nb,
   for (int J = 0; J < n; J += nb) {
     const int w = min(nb, n - J);
     if ((e = lu_panel(k, n, A, J, w, d_swaps, ws, s)) != cudaSuccess) return e;
-    if ((e = lu_laswp(k, A, J, w, 0, J, J + w, n, d_swaps, ws.status, s)) !=
+    if ((e = lu_laswp(k, A, 0, J, J + w, n, ws.swap_list, ws.status, s)) !=
         cudaSuccess)
       return e;
     const int rest = n - J - w;
@@ -338,6 +311,10 @@ cudaError_t LuWork::init(int sms) {
   if ((e = cudaMalloc(&rowj_words, jw)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&epoch, sizeof(unsigned))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&status, sizeof(int32_t))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&swap_list, (4 * LU_MAX_W + 1) * sizeof(int32_t))) !=
+      cudaSuccess)
+    return e;
+  cudaMemset(swap_list, 0, (4 * LU_MAX_W + 1) * sizeof(int32_t));
   cudaMemset(cand_words, 0, cw);
   cudaMemset(row_words, 0, rwb);
   cudaMemset(rowj_words, 0, jw);
@@ -373,17 +350,17 @@ cudaError_t lu_panel(int k, int n, MatView A, int J, int w, int32_t *d_swaps,
   return e;
 }
 
-cudaError_t lu_laswp(int k, MatView A, int J, int w, int c0, int c1, int c2,
-                     int c3, const int32_t *d_swaps, const int32_t *status,
+cudaError_t lu_laswp(int k, MatView A, int c0, int c1, int c2, int c3,
+                     const int32_t *swap_list, const int32_t *status,
                      cudaStream_t s) {
   int ncols = (c1 - c0) + (c3 - c2);
   if (ncols <= 0) return cudaSuccess;
   prof_begin(PROF_LASWP, s);
-  int blocks = (ncols * k + 255) / 256;
+  int blocks = (ncols * k + 127) / 128;
   switch (k) {
-    case 2: laswp_kernel<2><<<blocks, 256, 0, s>>>(A, J, w, c0, c1, c2, c3, d_swaps, status); break;
-    case 3: laswp_kernel<3><<<blocks, 256, 0, s>>>(A, J, w, c0, c1, c2, c3, d_swaps, status); break;
-    case 4: laswp_kernel<4><<<blocks, 256, 0, s>>>(A, J, w, c0, c1, c2, c3, d_swaps, status); break;
+    case 2: laswp_kernel<2><<<blocks, 128, 0, s>>>(A, c0, c1, c2, c3, swap_list, status); break;
+    case 3: laswp_kernel<3><<<blocks, 128, 0, s>>>(A, c0, c1, c2, c3, swap_list, status); break;
+    case 4: laswp_kernel<4><<<blocks, 128, 0, s>>>(A, c0, c1, c2, c3, swap_list, status); break;
     default: return cudaErrorInvalidValue;
   }
   prof_end(PROF_LASWP, s);

@@ -67,6 +67,7 @@ struct PanelSmem {
   int cand_row;    // this CTA's candidate for the next column
   int flag;        // 1 singular / last column: stop after B_WIN
   int singular;    // 1: stop without write-back
+  int piv[LU_MAX_W];                 // winner of every column of the panel
 };
 
 template <int K, int W>
@@ -178,9 +179,11 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       const int j = J + jj, par = jj & 1;
       const unsigned seq = seq0 + jj;
       trace(jj, 0);
-      // one round trip: every slot's index, |head| and pivot value
+      // every slot's index and |head| (the winner's pivot value is read
+      // afterwards: polling it from every slot costs more in L2 traffic
+      // than the extra, already-landed, round trip)
       constexpr int SPL = 5;        // slots per lane (G <= 160)
-      constexpr int NW = 3 + 2 * K; // words per slot
+      constexpr int NW = 3;         // words per slot polled here
       u64 wv[SPL][NW];
       unsigned done = 0;  // bit q: slot lane+32q complete (or absent)
 #pragma unroll
@@ -199,16 +202,11 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
 #pragma unroll
         for (int q = 0; q < SPL; ++q) {
           if (!(done & (1u << q))) {
-            bool head = true, piv = true;
+            bool head = true;
 #pragma unroll
             for (int x = 0; x < 3; ++x)
               if ((unsigned)wv[q][x] != seq) head = false;
-#pragma unroll
-            for (int x = 3; x < NW; ++x)
-              if ((unsigned)wv[q][x] != seq) piv = false;
-            // a CTA without rows >= j publishes no pivot value
-            if (head && ((int)(wv[q][0] >> 32) == INT_MAX || piv))
-              done |= 1u << q;
+            if (head) done |= 1u << q;
           }
         }
         if (__all_sync(0xffffffffu, done == (1u << SPL) - 1u)) break;
@@ -231,26 +229,21 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       trace(jj, 1);
       const int gw = (r - J) / R;
       if (g == 0 && lane == 0) swaps[j] = r;
-      // pivot value of the winner: already in lane gw%32, slot gw/32
-      const int wq = gw >> 5, wl = gw & 31;
+      // pivot value of the winner: lanes 0..2K-1 read its words
+      const u64 *pw = ws.cand_words + ((int64_t)par * G + gw) * LU_CAND_WORDS;
+      unsigned half = lane < 2 * K ? poll(pw + 3 + lane, seq) : 0u;
       double pv[K];
 #pragma unroll
       for (int c = 0; c < K; ++c) {
-        u64 lw = 0, hw = 0;
-#pragma unroll
-        for (int q = 0; q < SPL; ++q)
-          if (q == wq) {
-            lw = wv[q][3 + 2 * c];
-            hw = wv[q][4 + 2 * c];
-          }
-        unsigned l = __shfl_sync(0xffffffffu, (unsigned)(lw >> 32), wl);
-        unsigned h = __shfl_sync(0xffffffffu, (unsigned)(hw >> 32), wl);
+        unsigned l = __shfl_sync(0xffffffffu, half, 2 * c);
+        unsigned h = __shfl_sync(0xffffffffu, half, 2 * c + 1);
         pv[c] = __longlong_as_double((long long)(((u64)h << 32) | l));
       }
       const bool singular = pv[0] == 0.0;
       const bool last = (j == n - 1);
       if (lane == 0) {
         S.winner = r;
+        S.piv[jj] = r;
         S.gw = gw;
         S.flag = (singular || last) ? 1 : 0;
         S.singular = singular ? 1 : 0;
@@ -362,5 +355,43 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
 #pragma unroll
     for (int c = 0; c < K; ++c)
       A.p[c * A.plane + (int64_t)(rbeg + r) * A.ld + J + col] = at(r, col)[c];
+  }
+  // Epilogue: CTA 0 composes the panel's row exchanges for laswp_kernel
+  // (after the exchanges row cur[i] holds what row src[i] held before).
+  if (g == 0 && tid < 32) {
+    int ec0 = -1, es0 = -1, ec1 = -1, es1 = -1;  // lane entries l and l+32
+    int cnt = 0;
+    for (int jj = 0; jj < w; ++jj) {
+      const int a = J + jj, b = S.piv[jj];
+      if (a == b) continue;
+      unsigned fa = __ballot_sync(0xffffffffu, ec0 == a);
+      unsigned fa1 = __ballot_sync(0xffffffffu, ec1 == a);
+      unsigned fb = __ballot_sync(0xffffffffu, ec0 == b);
+      unsigned fb1 = __ballot_sync(0xffffffffu, ec1 == b);
+      int ia = fa ? __ffs(fa) - 1 : (fa1 ? 32 + __ffs(fa1) - 1 : -1);
+      int ib = fb ? __ffs(fb) - 1 : (fb1 ? 32 + __ffs(fb1) - 1 : -1);
+      if (ia < 0) {
+        ia = cnt++;
+        if (lane == (ia & 31)) {
+          if (ia < 32) { ec0 = a; es0 = a; } else { ec1 = a; es1 = a; }
+        }
+      }
+      if (ib < 0) {
+        ib = cnt++;
+        if (lane == (ib & 31)) {
+          if (ib < 32) { ec0 = b; es0 = b; } else { ec1 = b; es1 = b; }
+        }
+      }
+      int sa = __shfl_sync(0xffffffffu, ia < 32 ? es0 : es1, ia & 31);
+      int sb = __shfl_sync(0xffffffffu, ib < 32 ? es0 : es1, ib & 31);
+      if (lane == (ia & 31)) { if (ia < 32) es0 = sb; else es1 = sb; }
+      if (lane == (ib & 31)) { if (ib < 32) es0 = sa; else es1 = sa; }
+    }
+    if (lane < cnt) { ws.swap_list[lane] = ec0; ws.swap_list[64 + lane] = es0; }
+    if (lane + 32 < cnt) {
+      ws.swap_list[lane + 32] = ec1;
+      ws.swap_list[64 + lane + 32] = es1;
+    }
+    if (lane == 0) ws.swap_list[128] = cnt;
   }
 }
