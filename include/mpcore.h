@@ -137,6 +137,47 @@ int32_t mpcore_solve_ls_pm(int32_t k, int32_t n, const double *lu_planes,
                            const int32_t *swaps, const double *b_planes,
                            double *x_planes);
 
+/* ---- extensions: device-pointer building blocks (expert) ---------------
+ * For hosts that lay out and move device memory themselves -- the
+ * column-block-cyclic distributed LU (paper_2107_12550_b200/dist.py).
+ * Pointers are device addresses of planar views (base, ld, plane stride,
+ * all in elements); they are not checked beyond NULL. */
+
+/* device address of a matrix/vector object's planes */
+int32_t mpcore_object_device_ptr(uint64_t h, uint64_t *ptr);
+/* in-place LU with partial pivoting of an m x ncols block (ncols <= m):
+ * pivots over all m rows, exchanges rows inside the block only; swaps_out
+ * (host, ncols) are row indices relative to the block (linalg.py:422-449) */
+int32_t mpcore_dev_lu_block(int32_t k, int32_t m, int32_t ncols, uint64_t base,
+                            int64_t ld, int64_t plane, int32_t nb,
+                            int32_t *swaps_out, int32_t *singular_step);
+/* row exchanges (row0+i) <-> swaps[i], i ascending, on columns
+ * [col0, col0+ncols) of the view (linalg.py:430-431) */
+int32_t mpcore_dev_laswp(int32_t k, uint64_t base, int64_t ld, int64_t plane,
+                         int32_t col0, int32_t ncols, int32_t row0,
+                         const int32_t *swaps, int32_t nswaps);
+/* U <- L11^-1 U for unit-lower L11 (w x w) and U (w x ncols), each element
+ * continuing its chain add(u, mul(-l, u')) in ascending order */
+int32_t mpcore_dev_trsm(int32_t k, int32_t w, int32_t ncols, uint64_t l11,
+                        int64_t ldl, int64_t planel, uint64_t u12, int64_t ldu,
+                        int64_t planeu);
+/* C <- fold_p add(C, mul(opA(A_ip), B_pj)), opA = -A if neg_a, C from 0 if
+ * zero_init (linalg.py:577-617 and the LU trailing update) */
+int32_t mpcore_dev_gemm(int32_t k, int32_t neg_a, int32_t zero_init, int32_t M,
+                        int32_t N, int32_t Kd, uint64_t a, int64_t lda,
+                        int64_t pa, uint64_t b, int64_t ldb, int64_t pb,
+                        uint64_t c, int64_t ldc, int64_t pc);
+/* strided rows x cols copy of every plane */
+int32_t mpcore_dev_copy2d(int32_t k, int32_t rows, int32_t cols, uint64_t dst,
+                          int64_t ldd, int64_t pd, uint64_t src, int64_t lds,
+                          int64_t ps);
+/* the seeded recipe on the local columns of a column-block-cyclic layout */
+int32_t mpcore_dev_generate_cyclic(int32_t k, uint64_t base, int64_t ld,
+                                   int64_t plane, int32_t rows,
+                                   int32_t local_cols, int32_t nb,
+                                   int32_t world, int32_t rank, int32_t slot,
+                                   int64_t system_n, uint64_t seed);
+
 /* ---- extensions: device, diagnostics, profiling ------------------------ */
 
 /* select the CUDA device for this process (before any other call) */

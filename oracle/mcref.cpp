@@ -266,6 +266,99 @@ static int lu(int n, double *d, int32_t *swaps, int32_t *sing) {
   return 0;
 }
 
+// _lu_lanes restricted to an m x w block (row stride ld, plane stride pl):
+// pivot over all m rows, exchange rows inside the block, update inside the
+// block only.  The blocked/distributed factorisations are checked against
+// compositions of this, trsm() and gemm_update() (all in the reference's
+// per-element chain order).
+template <int K>
+static int lu_block(int m, int w, double *d, int64_t ld, int64_t pl,
+                    int32_t *swaps, int32_t *sing) {
+  double one[K] = {1.0};
+  for (int j = 0; j < w; ++j) {
+    int r = j;
+    double best = std::fabs(d[(int64_t)j * ld + j]);
+    for (int i = j + 1; i < m; ++i) {
+      double v = std::fabs(d[(int64_t)i * ld + j]);
+      if (v > best) { best = v; r = i; }
+    }
+    if (r != j)
+      for (int c = 0; c < K; ++c)
+        for (int q = 0; q < w; ++q)
+          std::swap(d[c * pl + (int64_t)j * ld + q], d[c * pl + (int64_t)r * ld + q]);
+    swaps[j] = r;
+    if (d[(int64_t)j * ld + j] == 0.0) { *sing = j; return 3; }
+    if (j + 1 == m) break;
+    double piv[K], recip[K];
+    for (int c = 0; c < K; ++c) piv[c] = d[c * pl + (int64_t)j * ld + j];
+    divk<K>(one, piv, recip);
+#pragma omp parallel for schedule(static) if (m - j > 256)
+    for (int i = j + 1; i < m; ++i) {
+      double a[K], mm[K], negm[K];
+      for (int c = 0; c < K; ++c) a[c] = d[c * pl + (int64_t)i * ld + j];
+      mul<K>(a, recip, mm);
+      for (int c = 0; c < K; ++c) {
+        d[c * pl + (int64_t)i * ld + j] = mm[c];
+        negm[c] = -mm[c];
+      }
+      for (int q = j + 1; q < w; ++q) {
+        double u[K], t[K], x[K], o[K];
+        for (int c = 0; c < K; ++c) {
+          u[c] = d[c * pl + (int64_t)j * ld + q];
+          x[c] = d[c * pl + (int64_t)i * ld + q];
+        }
+        mul<K>(negm, u, t);
+        add<K>(x, t, o);
+        for (int c = 0; c < K; ++c) d[c * pl + (int64_t)i * ld + q] = o[c];
+      }
+    }
+  }
+  return 0;
+}
+
+// U (w x ncols) <- chains add(U_jc, mul(-L_jt, U_tc)), t ascending (t < j)
+template <int K>
+static void trsm(int w, int ncols, const double *l, int64_t ldl, int64_t pl,
+                 double *u, int64_t ldu, int64_t pu) {
+#pragma omp parallel for schedule(static) if (ncols > 64)
+  for (int q = 0; q < ncols; ++q)
+    for (int j = 1; j < w; ++j)
+      for (int t = 0; t < j; ++t) {
+        double a[K], b[K], x[K], tt[K], o[K];
+        for (int c = 0; c < K; ++c) {
+          a[c] = -l[c * pl + (int64_t)j * ldl + t];
+          b[c] = u[c * pu + (int64_t)t * ldu + q];
+          x[c] = u[c * pu + (int64_t)j * ldu + q];
+        }
+        mul<K>(a, b, tt);
+        add<K>(x, tt, o);
+        for (int c = 0; c < K; ++c) u[c * pu + (int64_t)j * ldu + q] = o[c];
+      }
+}
+
+// C (M x N) <- fold_p add(C_ij, mul(-A_ip, B_pj)), p ascending
+template <int K>
+static void gemm_update(int M, int N, int KK, const double *a, int64_t lda,
+                        int64_t pa, const double *b, int64_t ldb, int64_t pb,
+                        double *cm, int64_t ldc, int64_t pc) {
+#pragma omp parallel for schedule(static) if (M > 16)
+  for (int i = 0; i < M; ++i)
+    for (int p = 0; p < KK; ++p) {
+      double x[K];
+      for (int c = 0; c < K; ++c) x[c] = -a[c * pa + (int64_t)i * lda + p];
+      for (int j = 0; j < N; ++j) {
+        double y[K], t[K], z[K], o[K];
+        for (int c = 0; c < K; ++c) {
+          y[c] = b[c * pb + (int64_t)p * ldb + j];
+          z[c] = cm[c * pc + (int64_t)i * ldc + j];
+        }
+        mul<K>(x, y, t);
+        add<K>(z, t, o);
+        for (int c = 0; c < K; ++c) cm[c * pc + (int64_t)i * ldc + j] = o[c];
+      }
+    }
+}
+
 // _solve_lanes (linalg.py:496-521); x holds b on entry.
 template <int K>
 static void solve(int n, const double *d, const int32_t *swaps, double *x) {
@@ -444,6 +537,24 @@ int mcref_matvec(int k, int rows, int cols, const double *a, const double *x,
 int mcref_gemm(int k, int m, int kk, int nn, const double *a, const double *b,
                double *c) {
   DISPATCH(k, gemm<K>(m, kk, nn, a, b, c));
+  return 0;
+}
+int mcref_lu_block(int k, int m, int w, double *a, int64_t ld, int64_t pl,
+                   int32_t *swaps, int32_t *sing_step) {
+  int st = 0;
+  *sing_step = -1;
+  DISPATCH(k, st = lu_block<K>(m, w, a, ld, pl, swaps, sing_step));
+  return st;
+}
+int mcref_trsm(int k, int w, int ncols, const double *l, int64_t ldl,
+               int64_t pl, double *u, int64_t ldu, int64_t pu) {
+  DISPATCH(k, trsm<K>(w, ncols, l, ldl, pl, u, ldu, pu));
+  return 0;
+}
+int mcref_gemm_update(int k, int M, int N, int KK, const double *a,
+                      int64_t lda, int64_t pa, const double *b, int64_t ldb,
+                      int64_t pb, double *c, int64_t ldc, int64_t pc) {
+  DISPATCH(k, gemm_update<K>(M, N, KK, a, lda, pa, b, ldb, pb, c, ldc, pc));
   return 0;
 }
 int mcref_num_threads(void) {

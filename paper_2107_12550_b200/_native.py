@@ -71,6 +71,22 @@ _PROTOS = {
     "mpcore_prof_read": (_i32, [_dp, ctypes.POINTER(_i64), _i32]),
     "mpcore_fp64_peak": (_i32, [_dp, _dp]),
     "mpcore_debug_panel_trace": (_i32, [ctypes.POINTER(_u64), _i64]),
+    # device-pointer building blocks (dist.py)
+    "mpcore_object_device_ptr": (_i32, [_u64, ctypes.POINTER(_u64)]),
+    "mpcore_dev_lu_block": (_i32, [_i32, _i32, _i32, _u64, _i64, _i64, _i32,
+                                   _ip, _ip]),
+    "mpcore_dev_laswp": (_i32, [_i32, _u64, _i64, _i64, _i32, _i32, _i32,
+                                _ip, _i32]),
+    "mpcore_dev_trsm": (_i32, [_i32, _i32, _i32, _u64, _i64, _i64, _u64,
+                               _i64, _i64]),
+    "mpcore_dev_gemm": (_i32, [_i32, _i32, _i32, _i32, _i32, _i32, _u64,
+                               _i64, _i64, _u64, _i64, _i64, _u64, _i64,
+                               _i64]),
+    "mpcore_dev_copy2d": (_i32, [_i32, _i32, _i32, _u64, _i64, _i64, _u64,
+                                 _i64, _i64]),
+    "mpcore_dev_generate_cyclic": (_i32, [_i32, _u64, _i64, _i64, _i32, _i32,
+                                          _i32, _i32, _i32, _i32, _i64,
+                                          _u64]),
 }
 
 # The 16 symbols of the reference ABI (build_lib.py:31-57).

@@ -292,7 +292,7 @@ int factor_locked(const ObjPtr &o, int nb, std::vector<int32_t> &swaps,
     D.swaps_cap = n;
   }
   int32_t step = -1;
-  e = mpk::lu_factor(o->k, n, view(o), D.dswaps,
+  e = mpk::lu_factor(o->k, n, n, view(o), D.dswaps,
                      nb > 0 ? nb : default_nb(o->k, n), D.ws, &step, D.stream);
   if (e != cudaSuccess) return cuda_fail(e, "lu_factor");
   swaps.assign(n, 0);
@@ -907,6 +907,196 @@ int32_t mpcore_prof_read(double *ms, int64_t *launches, int32_t cap) {
     launches[i] = P.launches[i];
   }
   return MPCORE_OK;
+}
+
+// ------------------------------------------ device-pointer (expert) API ----
+// Building blocks for callers that lay out and move device memory
+// themselves (the distributed LU in dist.py).  Pointers are device
+// addresses; views are planar (base, row stride, plane stride).
+
+static mpk::MatView mv(uint64_t base, int64_t ld, int64_t plane) {
+  mpk::MatView v;
+  v.p = reinterpret_cast<double *>(base);
+  v.ld = ld;
+  v.plane = plane;
+  return v;
+}
+
+static const int32_t *never_singular() {
+  static int32_t *d = nullptr;
+  if (!d) {
+    cudaMalloc(&d, sizeof(int32_t));
+    cudaMemset(d, 0xFF, sizeof(int32_t));
+    cudaDeviceSynchronize();
+  }
+  return d;
+}
+
+int32_t mpcore_object_device_ptr(uint64_t h, uint64_t *ptr) {
+  ObjPtr o = container(h);
+  if (!o) return MPCORE_BAD_HANDLE;
+  if (!ptr) return MPCORE_BAD_DIMENSION;
+  *ptr = reinterpret_cast<uint64_t>(o->d);
+  return MPCORE_OK;
+}
+
+int32_t mpcore_dev_lu_block(int32_t k, int32_t m, int32_t ncols, uint64_t base,
+                            int64_t ld, int64_t plane, int32_t nb,
+                            int32_t *swaps_out, int32_t *singular_step) {
+  if (k < 2 || k > 4 || m < 1 || ncols < 1 || ncols > m || !base ||
+      !swaps_out)
+    return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  Device &D = device();
+  cudaError_t e;
+  if (D.swaps_cap < ncols) {
+    if (D.dswaps) cudaFree(D.dswaps);
+    D.dswaps = nullptr;
+    D.swaps_cap = 0;
+    if ((e = cudaMalloc(&D.dswaps, (size_t)ncols * sizeof(int32_t))) !=
+        cudaSuccess)
+      return cuda_fail(e, "cudaMalloc(swaps)");
+    D.swaps_cap = ncols;
+  }
+  int32_t step = -1;
+  e = mpk::lu_factor(k, m, ncols, mv(base, ld, plane), D.dswaps,
+                     nb > 0 ? nb : 32, D.ws, &step, D.stream);
+  if (e != cudaSuccess) return cuda_fail(e, "lu_block");
+  e = cudaMemcpyAsync(swaps_out, D.dswaps, (size_t)ncols * sizeof(int32_t),
+                      cudaMemcpyDeviceToHost, D.stream);
+  int st = finish("lu_block");
+  if (st) return st;
+  if (e != cudaSuccess) return cuda_fail(e, "swaps download");
+  if (singular_step) *singular_step = step;
+  if (step >= 0)
+    return fail(MPCORE_SINGULAR,
+                "no nonzero pivot at elimination step " + std::to_string(step));
+  return MPCORE_OK;
+}
+
+int32_t mpcore_dev_laswp(int32_t k, uint64_t base, int64_t ld, int64_t plane,
+                         int32_t col0, int32_t ncols, int32_t row0,
+                         const int32_t *swaps, int32_t nswaps) {
+  if (k < 2 || k > 4 || !base || (nswaps > 0 && !swaps) || ncols < 0)
+    return MPCORE_BAD_DIMENSION;
+  if (nswaps <= 0 || ncols == 0) return MPCORE_OK;
+  DevLock L;
+  if (L.st) return L.st;
+  Device &D = device();
+  const int W = mpk::LU_MAX_W, LIST = 4 * W + 1;
+  const int chunks = (nswaps + W - 1) / W;
+  std::vector<int32_t> host((size_t)chunks * LIST, 0);
+  for (int ch = 0; ch < chunks; ++ch) {
+    // compose this chunk's exchanges: row cur[i] receives row src[i]
+    int32_t *cur = &host[(size_t)ch * LIST], *src = cur + 2 * W;
+    int cnt = 0;
+    for (int i = ch * W; i < std::min(nswaps, (ch + 1) * W); ++i) {
+      const int a = row0 + i, b = swaps[i];
+      if (a == b) continue;
+      int ia = -1, ib = -1;
+      for (int t = 0; t < cnt; ++t) {
+        if (cur[t] == a) ia = t;
+        if (cur[t] == b) ib = t;
+      }
+      if (ia < 0) { cur[cnt] = a; src[cnt] = a; ia = cnt++; }
+      if (ib < 0) { cur[cnt] = b; src[cnt] = b; ib = cnt++; }
+      std::swap(src[ia], src[ib]);
+    }
+    cur[4 * W] = cnt;
+  }
+  int32_t *dlist = nullptr;
+  cudaError_t e = cudaMallocAsync(&dlist, host.size() * sizeof(int32_t),
+                                  D.stream);
+  if (e != cudaSuccess) return cuda_fail(e, "laswp list");
+  e = cudaMemcpyAsync(dlist, host.data(), host.size() * sizeof(int32_t),
+                      cudaMemcpyHostToDevice, D.stream);
+  for (int ch = 0; ch < chunks && e == cudaSuccess; ++ch)
+    e = mpk::lu_laswp(k, mv(base, ld, plane), col0, col0 + ncols, 0, 0,
+                      dlist + (size_t)ch * LIST, never_singular(), D.stream);
+  cudaFreeAsync(dlist, D.stream);
+  if (e != cudaSuccess) return cuda_fail(e, "laswp");
+  return finish("laswp");
+}
+
+int32_t mpcore_dev_trsm(int32_t k, int32_t w, int32_t ncols, uint64_t l11,
+                        int64_t ldl, int64_t planel, uint64_t u12, int64_t ldu,
+                        int64_t planeu) {
+  if (k < 2 || k > 4 || w < 1 || ncols < 0 || !l11 || !u12)
+    return MPCORE_BAD_DIMENSION;
+  if (ncols == 0) return MPCORE_OK;
+  DevLock L;
+  if (L.st) return L.st;
+  Device &D = device();
+  const int W = mpk::LU_MAX_W;
+  cudaError_t e = cudaSuccess;
+  // blocked: each diagonal 32-block by the wavefront kernel, then the rows
+  // below it in the block get that block's contributions (ascending order)
+  for (int sb = 0; sb < w && e == cudaSuccess; sb += W) {
+    const int wb = std::min(W, w - sb);
+    mpk::MatView Ld = mv(l11 + (uint64_t)((sb * ldl + sb) * 8), ldl, planel);
+    mpk::MatView Us = mv(u12 + (uint64_t)(sb * ldu * 8), ldu, planeu);
+    e = mpk::lu_trsm(k, Ld, Us, wb, ncols, never_singular(), D.stream);
+    if (e == cudaSuccess && sb + wb < w) {
+      mpk::MatView L21 = mv(l11 + (uint64_t)(((sb + wb) * ldl + sb) * 8), ldl,
+                            planel);
+      mpk::MatView Ub = mv(u12 + (uint64_t)((sb + wb) * ldu * 8), ldu, planeu);
+      e = mpk::lu_update(k, w - sb - wb, ncols, wb, L21, Us, Ub,
+                         never_singular(), D.stream);
+    }
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "trsm");
+  return finish("trsm");
+}
+
+int32_t mpcore_dev_gemm(int32_t k, int32_t neg_a, int32_t zero_init, int32_t M,
+                        int32_t N, int32_t Kd, uint64_t a, int64_t lda,
+                        int64_t pa, uint64_t b, int64_t ldb, int64_t pb,
+                        uint64_t c, int64_t ldc, int64_t pc) {
+  if (k < 2 || k > 4 || M < 0 || N < 0 || Kd < 0 || !a || !b || !c)
+    return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  cudaError_t e = mpk::gemm(k, neg_a != 0, zero_init != 0, M, N, Kd,
+                            mv(a, lda, pa), mv(b, ldb, pb), mv(c, ldc, pc),
+                            device().stream);
+  if (e != cudaSuccess) return cuda_fail(e, "gemm");
+  return finish("gemm");
+}
+
+int32_t mpcore_dev_copy2d(int32_t k, int32_t rows, int32_t cols, uint64_t dst,
+                          int64_t ldd, int64_t pd, uint64_t src, int64_t lds,
+                          int64_t ps) {
+  if (k < 1 || rows < 0 || cols < 0 || !dst || !src) return MPCORE_BAD_DIMENSION;
+  if (rows == 0 || cols == 0) return MPCORE_OK;
+  DevLock L;
+  if (L.st) return L.st;
+  cudaError_t e = cudaSuccess;
+  for (int c = 0; c < k && e == cudaSuccess; ++c)
+    e = cudaMemcpy2DAsync(reinterpret_cast<double *>(dst) + c * pd,
+                          (size_t)ldd * 8,
+                          reinterpret_cast<const double *>(src) + c * ps,
+                          (size_t)lds * 8, (size_t)cols * 8, (size_t)rows,
+                          cudaMemcpyDeviceToDevice, device().stream);
+  if (e != cudaSuccess) return cuda_fail(e, "copy2d");
+  return finish("copy2d");
+}
+
+int32_t mpcore_dev_generate_cyclic(int32_t k, uint64_t base, int64_t ld,
+                                   int64_t plane, int32_t rows,
+                                   int32_t local_cols, int32_t nb,
+                                   int32_t world, int32_t rank, int32_t slot,
+                                   int64_t system_n, uint64_t seed) {
+  if (k < 2 || k > 4 || !base || rows < 0 || local_cols < 0 || nb < 1 ||
+      world < 1 || rank < 0 || rank >= world || system_n < 1)
+    return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  cudaError_t e = mpk::generate_cyclic(k, mv(base, ld, plane), rows,
+                                       local_cols, nb, world, rank, slot,
+                                       system_n, seed, device().stream);
+  if (e != cudaSuccess) return cuda_fail(e, "generate_cyclic");
+  return finish("generate_cyclic");
 }
 
 }  // extern "C"

@@ -82,6 +82,40 @@ gen_kernel(double *__restrict__ out, int64_t count, int64_t plane,
   }
 }
 
+// The same recipe for the local columns of a column-block-cyclic layout:
+// local column lc of rank `rank` is global column
+// ((lc / nb) * world + rank) * nb + lc % nb of a size-n system.
+template <int K>
+__global__ void __launch_bounds__(EW_THREADS)
+gen_cyclic_kernel(double *__restrict__ out, int64_t ld, int64_t plane,
+                  int rows, int local_cols, int nb, int world, int rank,
+                  uint64_t base_index, int64_t n, uint64_t seed) {
+  const int64_t count = (int64_t)rows * local_cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / local_cols), lc = (int)(e % local_cols);
+    const int64_t gc = ((int64_t)(lc / nb) * world + rank) * nb + lc % nb;
+    double o[K];
+    if (gc < n) {
+      uint64_t idx = (base_index + (uint64_t)r * (uint64_t)n + (uint64_t)gc) * 4ull;
+      double raw[K], zero[K];
+      raw[0] = uniform_at(seed, idx);
+#pragma unroll
+      for (int c = 1; c < K; ++c)
+        raw[c] = __dmul_rn(__dmul_rn(raw[c - 1], 0x1p-53),
+                           uniform_at(seed, idx + c));
+#pragma unroll
+      for (int c = 0; c < K; ++c) zero[c] = 0.0;
+      mc::add<K>(raw, zero, o);
+    } else {
+#pragma unroll
+      for (int c = 0; c < K; ++c) o[c] = 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < K; ++c) out[c * plane + (int64_t)r * ld + lc] = o[c];
+  }
+}
+
 // mat_vec: one thread per row; the row chain runs over column tiles staged
 // through shared memory with coalesced loads.
 constexpr int MV_ROWS = 128;
@@ -206,6 +240,25 @@ cudaError_t generate(int k, double *out, int64_t count, int64_t plane,
                      int slot, int64_t n, uint64_t seed, cudaStream_t s) {
   if (count <= 0) return cudaSuccess;
   KSWITCH(k, gen_k<K>(out, count, plane, slot, n, seed, s));
+}
+
+template <int K>
+static cudaError_t gen_cyclic_k(MatView out, int rows, int local_cols, int nb,
+                                int world, int rank, int slot, int64_t n,
+                                uint64_t seed, cudaStream_t s) {
+  uint64_t base = (uint64_t)slot * (uint64_t)n * (uint64_t)n;
+  gen_cyclic_kernel<K><<<grid_for((int64_t)rows * local_cols), EW_THREADS, 0,
+                         s>>>(out.p, out.ld, out.plane, rows, local_cols, nb,
+                              world, rank, base, n, seed);
+  return cudaGetLastError();
+}
+
+cudaError_t generate_cyclic(int k, MatView out, int rows, int local_cols,
+                            int nb, int world, int rank, int slot, int64_t n,
+                            uint64_t seed, cudaStream_t s) {
+  if ((int64_t)rows * local_cols <= 0) return cudaSuccess;
+  KSWITCH(k, gen_cyclic_k<K>(out, rows, local_cols, nb, world, rank, slot, n,
+                             seed, s));
 }
 
 template <int K>

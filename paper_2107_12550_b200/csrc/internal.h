@@ -57,6 +57,10 @@ cudaError_t axpy(int k, int64_t n, const double *alpha, const double *x,
 // with plane stride `plane` (>= count)
 cudaError_t generate(int k, double *out, int64_t count, int64_t plane,
                      int slot, int64_t n, uint64_t seed, cudaStream_t s);
+// the recipe on the local columns of a column-block-cyclic layout
+cudaError_t generate_cyclic(int k, MatView out, int rows, int local_cols,
+                            int nb, int world, int rank, int slot, int64_t n,
+                            uint64_t seed, cudaStream_t s);
 // y = A x (mat_vec), A rows x cols
 cudaError_t matvec(int k, int rows, int cols, MatView A, const double *x,
                    double *y, cudaStream_t s);
@@ -64,10 +68,12 @@ cudaError_t matvec(int k, int rows, int cols, MatView A, const double *x,
 // 0 when zero_init
 cudaError_t gemm(int k, bool neg_a, bool zero_init, int M, int N, int KK,
                  MatView A, MatView B, MatView C, cudaStream_t s);
-// LU with partial pivoting in place; swaps (device, n entries).  Returns
-// cudaSuccess; *sing_step = first singular step or -1.  nb = panel width.
-cudaError_t lu_factor(int k, int n, MatView A, int32_t *d_swaps, int nb,
-                      LuWork &w, int32_t *sing_step, cudaStream_t s);
+// LU with partial pivoting in place of the m x ncols matrix A (ncols <= m;
+// ncols < m factors a tall block, exchanging rows inside it only); swaps
+// (device, ncols entries, row indices relative to A).  *sing_step = first
+// singular step or -1.  nb = panel width (<= 32).
+cudaError_t lu_factor(int k, int m, int ncols, MatView A, int32_t *d_swaps,
+                      int nb, LuWork &w, int32_t *sing_step, cudaStream_t s);
 // Flags for the pipelined triangular solves (epoch-tagged, per block).
 struct SolveWork {
   int *flags = nullptr;

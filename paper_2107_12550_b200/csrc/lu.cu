@@ -260,11 +260,11 @@ MatView sub(MatView A, int i, int j) {
 struct GraphKey {
   const double *p;
   int64_t ld, plane;
-  int k, n, nb;
+  int k, m, ncols, nb;
   const int32_t *swaps;
   bool operator==(const GraphKey &o) const {
     return p == o.p && ld == o.ld && plane == o.plane && k == o.k &&
-           n == o.n && nb == o.nb && swaps == o.swaps;
+           m == o.m && ncols == o.ncols && nb == o.nb && swaps == o.swaps;
   }
 };
 struct GraphCache {
@@ -275,23 +275,29 @@ struct GraphCache {
   std::vector<Entry> entries;
 };
 
-cudaError_t enqueue_lu(int k, int n, MatView A, int32_t *d_swaps, int nb,
-                       LuWork &ws, cudaStream_t s) {
+// LU of the m x ncols matrix A (ncols <= m): ncols == m is the square
+// factorisation; ncols < m factors a tall block (the distributed LU's
+// panel), pivoting over all m rows and exchanging rows inside the block.
+cudaError_t enqueue_lu(int k, int m, int ncols, MatView A, int32_t *d_swaps,
+                       int nb, LuWork &ws, cudaStream_t s) {
   cudaError_t e;
   if ((e = lu_begin(ws, s)) != cudaSuccess) return e;
-  for (int J = 0; J < n; J += nb) {
-    const int w = min(nb, n - J);
-    if ((e = lu_panel(k, n, A, J, w, d_swaps, ws, s)) != cudaSuccess) return e;
-    if ((e = lu_laswp(k, A, 0, J, J + w, n, ws.swap_list, ws.status, s)) !=
-        cudaSuccess)
+  for (int J = 0; J < ncols; J += nb) {
+    const int w = min(nb, ncols - J);
+    if ((e = lu_panel(k, m, A, J, w, d_swaps, ws, s)) != cudaSuccess) return e;
+    if ((e = lu_laswp(k, A, 0, J, J + w, ncols, ws.swap_list, ws.status,
+                      s)) != cudaSuccess)
       return e;
-    const int rest = n - J - w;
-    if (rest > 0) {
-      if ((e = lu_trsm(k, sub(A, J, J), sub(A, J, J + w), w, rest, ws.status,
-                       s)) != cudaSuccess)
+    const int rest_r = m - J - w, rest_c = ncols - J - w;
+    if (rest_c > 0) {
+      if ((e = lu_trsm(k, sub(A, J, J), sub(A, J, J + w), w, rest_c,
+                       ws.status, s)) != cudaSuccess)
         return e;
-      if ((e = lu_update(k, rest, rest, w, sub(A, J + w, J), sub(A, J, J + w),
-                         sub(A, J + w, J + w), ws.status, s)) != cudaSuccess)
+    }
+    if (rest_c > 0 && rest_r > 0) {
+      if ((e = lu_update(k, rest_r, rest_c, w, sub(A, J + w, J),
+                         sub(A, J, J + w), sub(A, J + w, J + w), ws.status,
+                         s)) != cudaSuccess)
         return e;
     }
   }
@@ -389,18 +395,19 @@ cudaError_t lu_trsm(int k, MatView L11, MatView U12, int w, int ncols,
   return e;
 }
 
-cudaError_t lu_factor(int k, int n, MatView A, int32_t *d_swaps, int nb,
-                      LuWork &ws, int32_t *sing_step, cudaStream_t s) {
+cudaError_t lu_factor(int k, int m, int ncols, MatView A, int32_t *d_swaps,
+                      int nb, LuWork &ws, int32_t *sing_step, cudaStream_t s) {
   cudaError_t e;
   if (nb > LU_MAX_W) nb = LU_MAX_W;
   if (nb < 1) nb = 1;
   static const bool no_graph = std::getenv("MPCORE_NO_GRAPH") != nullptr;
   if (prof_enabled() || no_graph) {
     // direct launches (per-kernel event timing needs them)
-    if ((e = enqueue_lu(k, n, A, d_swaps, nb, ws, s)) != cudaSuccess) return e;
+    if ((e = enqueue_lu(k, m, ncols, A, d_swaps, nb, ws, s)) != cudaSuccess)
+      return e;
   } else {
     GraphCache &gc = *static_cast<GraphCache *>(ws.graphs);
-    GraphKey key{A.p, A.ld, A.plane, k, n, nb, d_swaps};
+    GraphKey key{A.p, A.ld, A.plane, k, m, ncols, nb, d_swaps};
     cudaGraphExec_t exec = nullptr;
     for (auto &en : gc.entries)
       if (en.key == key) exec = en.exec;
@@ -409,7 +416,7 @@ cudaError_t lu_factor(int k, int n, MatView A, int32_t *d_swaps, int nb,
       if ((e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal)) !=
           cudaSuccess)
         return e;
-      cudaError_t ee = enqueue_lu(k, n, A, d_swaps, nb, ws, s);
+      cudaError_t ee = enqueue_lu(k, m, ncols, A, d_swaps, nb, ws, s);
       e = cudaStreamEndCapture(s, &graph);
       if (ee != cudaSuccess) return ee;
       if (e != cudaSuccess) return e;

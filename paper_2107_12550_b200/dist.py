@@ -1,0 +1,258 @@
+"""Distributed DD/TD/QD LU with partial pivoting: 1-D column-block-cyclic
+layout over G GPUs, panel + pivot broadcast (BASELINE config 4; SURVEY
+§2.4, §8(e)).
+
+Block column b (columns [b*nb, (b+1)*nb)) lives on rank b % G.  For each
+panel P (owner o = P % G):
+  1. o factors its tall block rows [J, n) x the panel's nb columns in place
+     (pivot search over all rows; libmpcore's blocked LU on the block);
+  2. o packs the factored block (L21 with L11/U11 on top) contiguously and
+     broadcasts it with the nb pivot indices (NCCL over NVLink via
+     torch.distributed, one process per GPU);
+  3. every rank applies the row exchanges, in order, to its local columns,
+     solves U12 = L11^-1 A12 on its trailing local columns and updates its
+     trailing block A22 <- fold_j add(A22, mul(-L21_j, U12_j)).
+Every matrix element sees the reference's chain of add(., mul(-m, u)) in
+the reference's order (linalg.py:422-449), so the factors and pivots are
+bitwise those of the single-GPU factorisation and of the reference.
+
+The orchestration below is backend-agnostic: DeviceBackend drives the GPU
+through libmpcore's device-pointer entry points; the CPU tests plug in a
+checker backend (tests/test_dist_gloo.py) and run the same protocol on gloo
+with world_size 2.  `local_ranks` lets one process act for several ranks
+(one GPU emulating G ranks serially, broadcast = sharing the buffer).
+"""
+
+import numpy as np
+
+from . import _native as nat
+from .errors import SingularMatrixError
+
+__all__ = ["Layout", "DeviceBackend", "TorchComm", "LocalComm",
+           "dist_lu_factor"]
+
+
+class Layout:
+    """1-D column-block-cyclic layout of an n x n matrix over `world` ranks."""
+
+    def __init__(self, n, nb, world):
+        self.n, self.nb, self.world = int(n), int(nb), int(world)
+        self.nblocks = (self.n + self.nb - 1) // self.nb
+
+    def owner(self, b):
+        return b % self.world
+
+    def width(self, b):
+        return min(self.nb, self.n - b * self.nb)
+
+    def blocks_of(self, rank):
+        return list(range(rank, self.nblocks, self.world))
+
+    def local_cols(self, rank):
+        return sum(self.width(b) for b in self.blocks_of(rank))
+
+    def local_offset(self, rank, b):
+        """Local column of block b's first column on its owner."""
+        assert self.owner(b) == rank
+        # every block before the globally last one is full
+        return (b // self.world) * self.nb
+
+    def trailing_start(self, rank, P):
+        """First local column of rank's blocks with global index > P."""
+        cnt = 0 if P < rank else (P - rank) // self.world + 1
+        return min(cnt * self.nb, self.local_cols(rank))
+
+    def global_columns(self, rank):
+        cols = []
+        for b in self.blocks_of(rank):
+            cols.extend(range(b * self.nb, b * self.nb + self.width(b)))
+        return np.array(cols, dtype=np.int64)
+
+
+class LocalComm:
+    """World of ranks all served by this process: broadcast shares the
+    owner's buffer (nothing moves)."""
+
+    def broadcast(self, buf, root):
+        return buf
+
+    def barrier(self):
+        pass
+
+
+class TorchComm:
+    """torch.distributed broadcast (NCCL for CUDA tensors, gloo for CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+
+    def broadcast(self, buf, root):
+        self.dist.broadcast(buf, src=root, group=self.group)
+        if buf.is_cuda:
+            import torch
+            torch.cuda.current_stream().synchronize()
+        return buf
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+
+class DeviceBackend:
+    """Local blocks and panel buffers as torch CUDA tensors (planar
+    (k, rows, cols) float64), compute through libmpcore."""
+
+    def __init__(self, k, device=None):
+        import torch
+        self.torch = torch
+        self.k = k
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.L = nat.lib()
+
+    # -- storage -----------------------------------------------------------
+    def alloc(self, rows, cols):
+        return self.torch.zeros((self.k, rows, cols), dtype=self.torch.float64,
+                                device=self.device)
+
+    def view(self, M, row0=0, col0=0):
+        """(base address, ld, plane) of element (row0, col0)."""
+        k, rows, cols = M.shape
+        return (M.data_ptr() + (row0 * cols + col0) * 8, cols, rows * cols)
+
+    def to_host(self, M):
+        return M.cpu().numpy()
+
+    def int_buffer(self, n):
+        return self.torch.zeros(n, dtype=self.torch.int32, device=self.device)
+
+    def ints_to_host(self, t):
+        return t.cpu().numpy()
+
+    def ints_from_host(self, t, arr):
+        t.copy_(self.torch.from_numpy(np.ascontiguousarray(arr, np.int32)))
+
+    # -- compute -----------------------------------------------------------
+    def sync(self):
+        self.torch.cuda.current_stream().synchronize()
+
+    def generate(self, M, layout, rank, slot, seed):
+        base, ld, plane = self.view(M)
+        self.sync()
+        nat.check(self.L.mpcore_dev_generate_cyclic(
+            self.k, base, ld, plane, M.shape[1], M.shape[2], layout.nb,
+            layout.world, rank, slot, layout.n, seed), "generate_cyclic")
+
+    def lu_block(self, M, row0, col0, width):
+        """Factor rows [row0, n) x cols [col0, col0+width) in place; returns
+        the swaps as absolute row indices."""
+        base, ld, plane = self.view(M, row0, col0)
+        m = M.shape[1] - row0
+        sw = np.zeros(width, dtype=np.int32)
+        step = nat._i32(-1)
+        self.sync()
+        st = self.L.mpcore_dev_lu_block(self.k, m, width, base, ld, plane, 0,
+                                        nat.iptr(sw), nat.ctypes.byref(step))
+        if st == nat.SINGULAR:
+            raise SingularMatrixError(
+                "no nonzero pivot at elimination step %d" % (row0 + step.value),
+                step=row0 + step.value)
+        nat.check(st, "lu_block")
+        return sw + row0
+
+    def pack(self, M, row0, col0, width, buf):
+        rows = M.shape[1] - row0
+        dst = buf[:, :rows, :width]
+        base_d, ldd, pd = buf.data_ptr(), buf.shape[2], buf.shape[1] * buf.shape[2]
+        base_s, lds, ps = self.view(M, row0, col0)
+        self.sync()
+        nat.check(self.L.mpcore_dev_copy2d(self.k, rows, width, base_d, ldd,
+                                           pd, base_s, lds, ps), "copy2d")
+        return dst
+
+    def laswp(self, M, col0, ncols, row0, swaps):
+        if ncols <= 0:
+            return
+        base, ld, plane = self.view(M)
+        sw = np.ascontiguousarray(swaps, dtype=np.int32)
+        self.sync()
+        nat.check(self.L.mpcore_dev_laswp(self.k, base, ld, plane, col0, ncols,
+                                          row0, nat.iptr(sw), len(sw)),
+                  "laswp")
+
+    def trsm(self, buf, w, M, row0, col0, ncols):
+        bl, ldl, pl = buf.data_ptr(), buf.shape[2], buf.shape[1] * buf.shape[2]
+        bu, ldu, pu = self.view(M, row0, col0)
+        self.sync()
+        nat.check(self.L.mpcore_dev_trsm(self.k, w, ncols, bl, ldl, pl, bu,
+                                         ldu, pu), "trsm")
+
+    def gemm_update(self, buf, w, M, row0, col0, ncols):
+        mrows = M.shape[1] - row0 - w
+        if mrows <= 0 or ncols <= 0:
+            return
+        ldb, pb = buf.shape[2], buf.shape[1] * buf.shape[2]
+        a = buf.data_ptr() + (w * ldb) * 8            # L21: rows w.. of buf
+        bu, ldu, pu = self.view(M, row0, col0)         # U12
+        bc, ldc, pc = self.view(M, row0 + w, col0)     # A22
+        self.sync()
+        nat.check(self.L.mpcore_dev_gemm(self.k, 1, 0, mrows, ncols, w, a, ldb,
+                                         pb, bu, ldu, pu, bc, ldc, pc),
+                  "gemm_update")
+
+
+def _local_ranges(layout, rank, P):
+    """Local column ranges of `rank` outside panel P's block."""
+    lc = layout.local_cols(rank)
+    if layout.owner(P) != rank:
+        return [(0, lc)]
+    off = layout.local_offset(rank, P)
+    w = layout.width(P)
+    return [(0, off), (off + w, lc - off - w)]
+
+
+def dist_lu_factor(backend, comm, layout, local):
+    """Factor the distributed matrix in place.
+
+    local: {rank: local block (backend storage)} for the ranks this process
+    serves (all of them under LocalComm).  Returns the global swap list
+    (swaps[j] = r, the reference's PivotRecord.swaps, linalg.py:348-354).
+    Raises SingularMatrixError(step) on every rank alike.
+    """
+    n, G = layout.n, layout.world
+    k = backend.k
+    swaps_all = np.zeros(n, dtype=np.int32)
+    buf = backend.alloc(n, layout.nb)
+    ibuf = backend.int_buffer(layout.nb + 1)
+    for P in range(layout.nblocks):
+        J, w, owner = P * layout.nb, layout.width(P), layout.owner(P)
+        status = np.zeros(layout.nb + 1, dtype=np.int32)
+        if owner in local:
+            M = local[owner]
+            off = layout.local_offset(owner, P)
+            try:
+                sw = backend.lu_block(M, J, off, w)
+                status[:w] = sw
+                status[layout.nb] = -1
+            except SingularMatrixError as e:
+                status[layout.nb] = e.step
+            backend.pack(M, J, off, w, buf)
+        backend.ints_from_host(ibuf, status)
+        comm.broadcast(ibuf, owner)            # pivots (+ singular flag)
+        status = backend.ints_to_host(ibuf)
+        if status[layout.nb] >= 0:
+            raise SingularMatrixError(
+                "no nonzero pivot at elimination step %d" % status[layout.nb],
+                step=int(status[layout.nb]))
+        comm.broadcast(buf, owner)             # factored panel L21 / L11 / U11
+        sw = status[:w].copy()
+        swaps_all[J:J + w] = sw
+        for rank, M in local.items():
+            for c0, nc in _local_ranges(layout, rank, P):
+                backend.laswp(M, c0, nc, J, sw)
+            t0 = layout.trailing_start(rank, P)
+            nt = layout.local_cols(rank) - t0
+            if nt > 0:
+                backend.trsm(buf, w, M, J, t0, nt)
+                backend.gemm_update(buf, w, M, J, t0, nt)
+    return swaps_all
