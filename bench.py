@@ -7,7 +7,7 @@ the same recipe, b = A*x_true in TD on the device).  A step = restore A
 (device-to-device copy of the pristine matrix, which also evicts L2:
 2 x 100 MB > 126 MB L2) + LU + solve.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--k 3] [--n 2048]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--k 3] [--dim 2048]
     python bench.py --impl reference ...   (CPU oracle port, all host threads)
 
 Multi-GPU (torchrun, one rank per GPU): independent replicas of the same
@@ -331,20 +331,145 @@ def run_ours(args):
     print(json.dumps(line))
 
 
+def run_dist(args):
+    """BASELINE config 4: distributed DD LU (+ solve) of one n x n system,
+    column-block-cyclic over the ranks (nb = 256), NCCL panel + pivot
+    broadcast; factors gathered to rank 0 for the solve.  Strong scaling:
+    the whole system is fixed, value = (2/3) n^3 / (max-over-ranks time)."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    os.environ.setdefault("MPCORE_DEVICE", str(local))
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local))
+    from paper_2107_12550_b200 import _native as nat
+    from paper_2107_12550_b200.dist import (DeviceBackend, Layout, TorchComm,
+                                            dist_lu_factor)
+    k, n, nb = args.k, args.n, args.dist_nb
+    seed = 210712550 + 4
+    layout = Layout(n, nb, world)
+    be = DeviceBackend(k)
+    lc = layout.local_cols(rank)
+    M = be.alloc(n, lc)
+    be.generate(M, layout, rank, 0, seed)
+    M0 = M.clone()
+    L = nat.lib()
+    if rank == 0:
+        # b = A x_true in DD (x_true = ones; config 0 recipe), full A
+        full = M if world == 1 else be.alloc(n, n)
+        if world > 1:
+            be.generate(full, Layout(n, nb, 1), 0, 0, seed)
+        xt = torch.zeros((k, n), dtype=torch.float64, device="cuda")
+        xt[0] = 1.0
+        b = torch.zeros_like(xt)
+        x = torch.zeros_like(xt)
+        torch.cuda.synchronize()
+        nat.check(L.mpcore_dev_matvec(k, n, n, full.data_ptr(), n, n * n,
+                                      xt.data_ptr(), b.data_ptr()), "matvec")
+    comm = TorchComm()
+    recv = be.alloc(n, layout.local_cols(1)) if (rank == 0 and world > 1) \
+        else None
+
+    def step():
+        M.copy_(M0)
+        torch.cuda.synchronize()
+        swaps = dist_lu_factor(be, comm, layout, {rank: M})
+        if world > 1:
+            if rank == 0:
+                full[:, :, torch.as_tensor(layout.global_columns(0),
+                                           device="cuda")] = M
+                for q in range(1, world):
+                    buf = recv[:, :, :layout.local_cols(q)].contiguous()
+                    dist.recv(buf, src=q)
+                    full[:, :, torch.as_tensor(layout.global_columns(q),
+                                               device="cuda")] = buf
+            else:
+                dist.send(M, dst=0)
+        if rank == 0:
+            torch.cuda.synchronize()
+            sw = np.ascontiguousarray(swaps, dtype=np.int32)
+            nat.check(L.mpcore_dev_lu_solve(k, n, full.data_ptr(), n, n * n,
+                                            nat.iptr(sw), b.data_ptr(),
+                                            x.data_ptr()), "solve")
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        wall = time.perf_counter() - t0
+    t = torch.tensor([wall], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) * 1e3 / args.steps
+    if rank == 0:
+        xs = x.cpu().numpy()
+        err = float(np.max(np.abs((xs[0] - 1.0) + xs[1])))
+        flops = (2.0 / 3.0) * n ** 3
+        wc = work_counts(n, k)
+        line = {
+            "metric": "%s LU+solve eff. GFLOP/s ((2/3)n^3/s)" % NAMES[k],
+            "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64x%d (%s, bit-exact EFT arithmetic)" % (k, NAMES[k]),
+            "data": "synthetic (seeded recipe, SURVEY 8d; seed %d)" % seed,
+            "config": {"workload": "config4: distributed %s LU+PP+solve n=%d"
+                       % (NAMES[k], n), "n": n, "k": k, "nb": nb,
+                       "parallelism": "column-block-cyclic x%d, NCCL panel "
+                       "+ pivot broadcast, gather + solve on rank 0" % world,
+                       "l2": "A restored from a pristine copy each step "
+                             "(>> L2)"},
+            "check": {"max_abs_err_x_vs_ones": err},
+            "roofline": {"bound": "fp64",
+                         "achieved": wc["instr"] / (ms * 1e-3) / 1e12 / world,
+                         "unit": "T FP64 instr/s per GPU",
+                         "peak": 18.2, "frac": wc["instr"] / (ms * 1e-3) /
+                         18.2e12 / world, "traffic": None},
+            "e2e": None, "gpu_launches": None,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--k", type=int, default=3)
-    ap.add_argument("--n", type=int, default=2048)
+    ap.add_argument("--config", type=int, default=2, choices=[2, 4])
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--dim", dest="n", type=int, default=None)
     ap.add_argument("--nb", type=int, default=0)
+    ap.add_argument("--dist-nb", type=int, default=256)
     ap.add_argument("--cpu-n", type=int, default=768)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.config == 4:
+        args.k = args.k or 2
+        args.n = args.n or 32768
+    else:
+        args.k = args.k or 3
+        args.n = args.n or 2048
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == 4:
+        run_dist(args)
     else:
         run_ours(args)
 

@@ -171,6 +171,14 @@ int32_t mpcore_dev_gemm(int32_t k, int32_t neg_a, int32_t zero_init, int32_t M,
 int32_t mpcore_dev_copy2d(int32_t k, int32_t rows, int32_t cols, uint64_t dst,
                           int64_t ldd, int64_t pd, uint64_t src, int64_t lds,
                           int64_t ps);
+/* x <- solve(LU, swaps, b) for device LU (n x n view), host swaps (n),
+ * device b and x (k*n, planar, not aliased) (linalg.py:496-538) */
+int32_t mpcore_dev_lu_solve(int32_t k, int32_t n, uint64_t lu, int64_t ld,
+                            int64_t plane, const int32_t *swaps, uint64_t b,
+                            uint64_t x);
+/* y <- A x (mat_vec, linalg.py:545-574) on device views; x, y planar k*n */
+int32_t mpcore_dev_matvec(int32_t k, int32_t rows, int32_t cols, uint64_t a,
+                          int64_t ld, int64_t plane, uint64_t x, uint64_t y);
 /* the seeded recipe on the local columns of a column-block-cyclic layout */
 int32_t mpcore_dev_generate_cyclic(int32_t k, uint64_t base, int64_t ld,
                                    int64_t plane, int32_t rows,

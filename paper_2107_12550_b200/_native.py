@@ -84,6 +84,10 @@ _PROTOS = {
                                _i64]),
     "mpcore_dev_copy2d": (_i32, [_i32, _i32, _i32, _u64, _i64, _i64, _u64,
                                  _i64, _i64]),
+    "mpcore_dev_lu_solve": (_i32, [_i32, _i32, _u64, _i64, _i64, _ip, _u64,
+                                   _u64]),
+    "mpcore_dev_matvec": (_i32, [_i32, _i32, _i32, _u64, _i64, _i64, _u64,
+                                 _u64]),
     "mpcore_dev_generate_cyclic": (_i32, [_i32, _u64, _i64, _i64, _i32, _i32,
                                           _i32, _i32, _i32, _i32, _i64,
                                           _u64]),

@@ -1082,6 +1082,47 @@ int32_t mpcore_dev_copy2d(int32_t k, int32_t rows, int32_t cols, uint64_t dst,
   return finish("copy2d");
 }
 
+int32_t mpcore_dev_lu_solve(int32_t k, int32_t n, uint64_t lu, int64_t ld,
+                            int64_t plane, const int32_t *swaps, uint64_t b,
+                            uint64_t x) {
+  if (k < 2 || k > 4 || n < 1 || !lu || !swaps || !b || !x || b == x)
+    return MPCORE_BAD_DIMENSION;
+  std::vector<int32_t> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  for (int j = 0; j < n; ++j) {
+    if (swaps[j] < j || swaps[j] >= n) return MPCORE_BAD_DIMENSION;
+    if (swaps[j] != j) std::swap(order[j], order[swaps[j]]);
+  }
+  DevLock L;
+  if (L.st) return L.st;
+  Device &D = device();
+  int32_t *dperm = nullptr;
+  cudaError_t e = cudaMallocAsync(&dperm, (size_t)n * sizeof(int32_t), D.stream);
+  if (e != cudaSuccess) return cuda_fail(e, "perm");
+  e = cudaMemcpyAsync(dperm, order.data(), (size_t)n * sizeof(int32_t),
+                      cudaMemcpyHostToDevice, D.stream);
+  if (e == cudaSuccess)
+    e = mpk::lu_solve(k, n, mv(lu, ld, plane), dperm,
+                      reinterpret_cast<const double *>(b),
+                      reinterpret_cast<double *>(x), D.sw, D.stream);
+  cudaFreeAsync(dperm, D.stream);
+  if (e != cudaSuccess) return cuda_fail(e, "dev_lu_solve");
+  return finish("dev_lu_solve");
+}
+
+int32_t mpcore_dev_matvec(int32_t k, int32_t rows, int32_t cols, uint64_t a,
+                          int64_t ld, int64_t plane, uint64_t x, uint64_t y) {
+  if (k < 2 || k > 4 || rows < 1 || cols < 1 || !a || !x || !y || x == y)
+    return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  cudaError_t e = mpk::matvec(k, rows, cols, mv(a, ld, plane),
+                              reinterpret_cast<const double *>(x),
+                              reinterpret_cast<double *>(y), device().stream);
+  if (e != cudaSuccess) return cuda_fail(e, "dev_matvec");
+  return finish("dev_matvec");
+}
+
 int32_t mpcore_dev_generate_cyclic(int32_t k, uint64_t base, int64_t ld,
                                    int64_t plane, int32_t rows,
                                    int32_t local_cols, int32_t nb,

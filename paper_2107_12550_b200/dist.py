@@ -137,6 +137,8 @@ class DeviceBackend:
         self.torch.cuda.current_stream().synchronize()
 
     def generate(self, M, layout, rank, slot, seed):
+        if M.numel() == 0:          # a rank without blocks (world > nblocks)
+            return
         base, ld, plane = self.view(M)
         self.sync()
         nat.check(self.L.mpcore_dev_generate_cyclic(
