@@ -145,22 +145,15 @@ gemm_kernel(int M, int N, int KK, MatView A, MatView B, MatView C,
     }
 }
 
-// Tile shapes per precision (first-cut; tuned with ncu on B200).
-template <int K> struct Tile;
-template <> struct Tile<2> {
-  static constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4, MINB = 1;
-};
-template <> struct Tile<3> {
-  static constexpr int BM = 32, BN = 32, BK = 16, TM = 2, TN = 2, MINB = 1;
-};
-template <> struct Tile<4> {
-  static constexpr int BM = 32, BN = 32, BK = 16, TM = 2, TN = 2, MINB = 1;
+template <int BM_, int BN_, int BK_, int TM_, int TN_, int MINB_>
+struct TileT {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, TM = TM_, TN = TN_,
+                       MINB = MINB_;
 };
 
-template <int K, bool NEG_A, bool ZERO>
-cudaError_t launch(int M, int N, int KK, MatView A, MatView B, MatView C,
-                   const int32_t *status, cudaStream_t s) {
-  using T = Tile<K>;
+template <int K, class T, bool NEG_A, bool ZERO>
+cudaError_t launch_t(int M, int N, int KK, MatView A, MatView B, MatView C,
+                     const int32_t *status, cudaStream_t s) {
   using Cfg = GemmCfg<K, T::BM, T::BN, T::BK, T::TM, T::TN>;
   auto kern = gemm_kernel<K, T::BM, T::BN, T::BK, T::TM, T::TN, NEG_A, ZERO,
                           T::MINB>;
@@ -174,6 +167,39 @@ cudaError_t launch(int M, int N, int KK, MatView A, MatView B, MatView C,
   dim3 grid((N + T::BN - 1) / T::BN, (M + T::BM - 1) / T::BM);
   kern<<<grid, Cfg::NT, Cfg::SMEM, s>>>(M, N, KK, A, B, C, status);
   return cudaGetLastError();
+}
+
+// Tile shapes per precision.  Variant 0 is the default; the others are
+// kept selectable (MPCORE_GEMM_VARIANT) for tuning sweeps on the B200.
+int gemm_variant() {
+  static const int v = [] {
+    const char *e = std::getenv("MPCORE_GEMM_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int K, bool NEG_A, bool ZERO>
+cudaError_t launch(int M, int N, int KK, MatView A, MatView B, MatView C,
+                   const int32_t *status, cudaStream_t s) {
+  const int v = gemm_variant();
+  if constexpr (K == 2) {
+    switch (v) {
+      case 1: return launch_t<K, TileT<64, 64, 16, 4, 4, 1>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
+      case 2: return launch_t<K, TileT<128, 64, 8, 8, 4, 1>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
+      case 3: return launch_t<K, TileT<64, 64, 8, 4, 4, 1>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
+      case 4: return launch_t<K, TileT<32, 64, 16, 2, 4, 2>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
+      default: return launch_t<K, TileT<64, 64, 16, 4, 4, 2>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
+    }
+  } else {
+    switch (v) {
+      case 1: return launch_t<K, TileT<32, 32, 16, 2, 2, 2>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
+      case 2: return launch_t<K, TileT<64, 32, 16, 4, 2, 1>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
+      case 3: return launch_t<K, TileT<32, 32, 8, 2, 2, 1>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
+      case 4: return launch_t<K, TileT<32, 16, 16, 2, 1, 2>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
+      default: return launch_t<K, TileT<32, 32, 16, 2, 2, 1>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
+    }
+  }
 }
 
 }  // namespace
