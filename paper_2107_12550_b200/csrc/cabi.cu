@@ -528,6 +528,95 @@ int32_t mpcore_lu_solve(uint64_t lu_h, uint64_t piv_h, uint64_t b_h,
 }
 
 // ------------------------------------------------------------- refine ----
+}  // extern "C"
+
+namespace {
+// The IR's short side on the GPU: factors stay resident in HBM.
+class GpuShortSolver : public mpr::ShortSolver {
+ public:
+  ~GpuShortSolver() override {
+    if (a_ || perm_ || b_ || x_) {
+      DevLock L;
+      if (a_) cudaFree(a_);
+      if (perm_) cudaFree(perm_);
+      if (b_) cudaFree(b_);
+      if (x_) cudaFree(x_);
+    }
+  }
+  int factor(int k, int n, const std::vector<double> &a,
+             std::string &err) override {
+    k_ = k;
+    n_ = n;
+    DevLock L;
+    if (L.st) { err = g_err; return L.st; }
+    Device &D = device();
+    cudaError_t e;
+    size_t mb = (size_t)k * n * n * sizeof(double), vb = (size_t)k * n * 8;
+    if ((e = cudaMalloc(&a_, mb)) != cudaSuccess ||
+        (e = cudaMalloc(&b_, vb)) != cudaSuccess ||
+        (e = cudaMalloc(&x_, vb)) != cudaSuccess ||
+        (e = cudaMalloc(&perm_, (size_t)n * 4)) != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
+    if ((e = cudaMemcpy(a_, a.data(), mb, cudaMemcpyHostToDevice)) !=
+        cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
+    auto o = std::make_shared<Object>();  // borrow the factor path
+    o->kind = K_MATRIX;
+    o->k = k;
+    o->rows = o->cols = n;
+    o->d = a_;
+    std::vector<int32_t> swaps;
+    int32_t step = -1;
+    int st = factor_locked(o, 0, swaps, &step);
+    o->d = nullptr;  // not owned
+    if (st) { err = g_err; return st; }
+    std::vector<int32_t> order(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    for (int j = 0; j < n; ++j)
+      if (swaps[j] != j) std::swap(order[j], order[swaps[j]]);
+    if ((e = cudaMemcpy(perm_, order.data(), (size_t)n * 4,
+                        cudaMemcpyHostToDevice)) != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
+    (void)D;
+    return MPCORE_OK;
+  }
+  int solve(const std::vector<double> &b, std::vector<double> &x,
+            std::string &err) override {
+    DevLock L;
+    if (L.st) { err = g_err; return L.st; }
+    Device &D = device();
+    size_t vb = (size_t)k_ * n_ * 8;
+    cudaError_t e = cudaMemcpyAsync(b_, b.data(), vb, cudaMemcpyHostToDevice,
+                                    D.stream);
+    mpk::MatView v{a_, n_, (int64_t)n_ * n_};
+    if (e == cudaSuccess)
+      e = mpk::lu_solve(k_, n_, v, perm_, b_, x_, D.sw, D.stream);
+    x.resize((size_t)k_ * n_);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(x.data(), x_, vb, cudaMemcpyDeviceToHost, D.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(D.stream);
+    if (e != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
+    return MPCORE_OK;
+  }
+
+ private:
+  int k_ = 0, n_ = 0;
+  double *a_ = nullptr, *b_ = nullptr, *x_ = nullptr;
+  int32_t *perm_ = nullptr;
+};
+}  // namespace
+
+extern "C" {
+
 int32_t mpcore_refine(const char *a_path, const char *b_path, int32_t short_k,
                       int32_t long_bits, const char *rtol, const char *atol,
                       int32_t max_iter, uint64_t *report_out) {
@@ -536,8 +625,9 @@ int32_t mpcore_refine(const char *a_path, const char *b_path, int32_t short_k,
   if (!a_path || !b_path || !rtol || !atol) return MPCORE_BAD_PARSE;
   auto rep = std::make_unique<mpr::Report>();
   std::string err;
+  GpuShortSolver gpu;
   int st = mpr::refine_files(a_path, b_path, short_k, long_bits, rtol, atol,
-                             max_iter, *rep, err);
+                             max_iter, gpu, *rep, err);
   if (st) return fail(st, err);
   auto o = std::make_shared<Object>();
   o->kind = K_REPORT;
@@ -579,7 +669,8 @@ int32_t mpcore_report_residual_entry(uint64_t h, int32_t idx, int32_t digits,
   if (!r) return MPCORE_BAD_HANDLE;
   if (idx < 0 || idx >= (int32_t)r->residuals.size())
     return MPCORE_BAD_DIMENSION;
-  return copy_text(mpr::format_decimal(r->residuals[idx], digits), out, cap);
+  return copy_text(mpr::format_decimal(r->residuals[idx], digits, r->prec), out,
+                   cap);
 }
 
 int32_t mpcore_report_solution_count(uint64_t h, int32_t *out) {
@@ -596,7 +687,8 @@ int32_t mpcore_report_solution_entry(uint64_t h, int32_t idx, int32_t digits,
   if (!r) return MPCORE_BAD_HANDLE;
   if (idx < 0 || idx >= (int32_t)r->solution.size())
     return MPCORE_BAD_DIMENSION;
-  return copy_text(mpr::format_decimal(r->solution[idx], digits), out, cap);
+  return copy_text(mpr::format_decimal(r->solution[idx], digits, r->prec), out,
+                   cap);
 }
 
 // --------------------------------------------------------- extensions ----

@@ -1,7 +1,8 @@
 // Host-side mixed-precision iterative refinement behind mpcore_refine
 // (ffi.py:243-258 -> refine.py:121-197): .mpmat loading (matfile.py), the
-// long-precision residual loop in correctly rounded big-float arithmetic, and
-// the short-precision factor/solve on the GPU.
+// long-precision residual loop in correctly rounded big-float arithmetic
+// (bignum.h; same single-rounding semantics as bigfloat.py), and the
+// short-precision factor/solve on the GPU through ShortSolver.
 #pragma once
 #include <cstdint>
 #include <string>
@@ -16,15 +17,37 @@ struct Report {
   std::string stop_reason = "max_iter";
   std::vector<bn::BF> residuals;   // residual 2-norm per iteration
   std::vector<bn::BF> solution;    // final x at long precision
-  int64_t prec = 0;
+  int64_t prec = 0;                // precision of residuals / solution
+};
+
+// The short side: factor once, solve many (implemented on the GPU by
+// cabi.cu).  Planes are k x n (vectors) / k x n x n (matrix), planar.
+class ShortSolver {
+ public:
+  virtual ~ShortSolver() = default;
+  // -> status (0 ok, 3 singular, 6 other)
+  virtual int factor(int k, int n, const std::vector<double> &a_planes,
+                     std::string &err) = 0;
+  virtual int solve(const std::vector<double> &b_planes,
+                    std::vector<double> &x_planes, std::string &err) = 0;
 };
 
 // -> status (0 ok, 2 dims, 3 singular, 4 parse/file, 5 overflow, 6 other)
 int refine_files(const char *a_path, const char *b_path, int short_k,
                  int long_bits, const char *rtol, const char *atol,
-                 int max_iter, Report &out, std::string &err);
+                 int max_iter, ShortSolver &short_side, Report &out,
+                 std::string &err);
 
-// bf_format_decimal (bigfloat.py:483-509); digits <= 0 = default for prec
-std::string format_decimal(const bn::BF &v, int digits, int64_t prec = 0);
+// bf_format_decimal (bigfloat.py:483-509); digits <= 0: the default for prec
+std::string format_decimal(const bn::BF &v, int digits, int64_t prec);
+
+// correctly rounded long arithmetic at precision p (bigfloat.py:239-326)
+bn::BF lf_add(const bn::BF &a, const bn::BF &b, int64_t p);
+bn::BF lf_sub(const bn::BF &a, const bn::BF &b, int64_t p);
+bn::BF lf_mul(const bn::BF &a, const bn::BF &b, int64_t p);
+bn::BF lf_div(const bn::BF &a, const bn::BF &b, int64_t p);
+bn::BF lf_sqrt(const bn::BF &a, int64_t p);
+bn::BF lf_round(const bn::BF &a, int64_t p);
+int lf_cmp(const bn::BF &a, const bn::BF &b);
 
 }  // namespace mpr

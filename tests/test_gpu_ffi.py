@@ -118,3 +118,60 @@ def test_rectangular_factor_is_dimension_error():
     h = new_matrix(3, 2, 3)
     assert ffi.lu_factor(h)[0] == ffi.BAD_DIMENSION
     ffi.release(h)
+
+
+# --------------------------------------------------------------- refine ----
+from paper_2107_12550_b200.longfloat import (format_decimal, format_hex,
+                                             parse_hex)
+
+
+def write_bf(path, rows_hex, bits):
+    with open(path, "w") as fh:
+        fh.write("mpmat %d %d bf %d\n" % (len(rows_hex), len(rows_hex[0]), bits))
+        for row in rows_hex:
+            fh.write(" ".join(row) + "\n")
+
+
+@pytest.mark.parametrize("idx", range(5))
+def test_native_refine_matches_reference(tmp_path, idx):
+    """mpcore_refine (ffi.py:243-258): native long arithmetic + GPU short
+    solves reproduce the reference's IR run bit for bit."""
+    case = G["refine"][idx]
+    p = case["long_bits"]
+    a_path, b_path = str(tmp_path / "A.mpmat"), str(tmp_path / "b.mpmat")
+    write_bf(a_path, case["A"], p)
+    write_bf(b_path, [[h] for h in case["b"]], p)
+    st, rep = ffi.refine(a_path, b_path, case["short_k"], p, case["rtol"], "0",
+                         40)
+    assert st == ffi.OK, st
+    assert ffi.report_iterations(rep) == (ffi.OK, case["iterations"])
+    assert ffi.report_stop_reason(rep) == (ffi.OK, case["stop_reason"])
+    st, count = ffi.report_residual_count(rep)
+    assert count == len(case["history"])
+    for i, h in enumerate(case["history"]):
+        want = format_decimal(parse_hex(h).round(p), 60)
+        assert ffi.report_residual_entry(rep, i, 60) == (ffi.OK, want)
+    for i, h in enumerate(case["solution"]):
+        v = parse_hex(h).round(p)
+        assert ffi.report_solution_entry(rep, i, 40) == (ffi.OK,
+                                                         format_decimal(v, 40))
+        # default digits: ceil(prec*log10 2)+2 (bigfloat.py:489-490)
+        assert ffi.report_solution_entry(rep, i, 0) == (ffi.OK,
+                                                        format_decimal(v))
+    assert ffi.report_residual_entry(rep, count, 20)[0] == ffi.BAD_DIMENSION
+    ffi.release(rep)
+    assert ffi.report_iterations(rep)[0] == ffi.BAD_HANDLE
+
+
+def test_native_refine_errors(tmp_path):
+    # test_ffi.py:204-215
+    st, rep = ffi.refine(str(tmp_path / "nope.mpmat"),
+                         str(tmp_path / "nope2.mpmat"), 2, 424, "1e-30", "0", 5)
+    assert (st, rep) == (ffi.BAD_PARSE, 0)
+    case = G["refine"][4]
+    a_path, b_path = str(tmp_path / "A.mpmat"), str(tmp_path / "b.mpmat")
+    write_bf(a_path, case["A"], case["long_bits"])
+    write_bf(b_path, [[h] for h in case["b"]], case["long_bits"])
+    assert ffi.refine(a_path, b_path, 7, 424, "1e-30", "0", 5) == (ffi.INTERNAL, 0)
+    assert ffi.refine(a_path, b_path, 2, 424, "abc", "0", 5)[0] == ffi.BAD_PARSE
+    assert ffi.refine(a_path, b_path, 2, 424, "0", "0", 5)[0] == ffi.INTERNAL
