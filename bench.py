@@ -73,29 +73,33 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.samples = []
-        self.stop = threading.Event()
-        self.t = threading.Thread(target=self.run, daemon=True)
-
-    def run(self):
-        while not self.stop.is_set():
-            try:
-                out = subprocess.run(
-                    ["nvidia-smi", "-i", str(self.index),
-                     "--query-gpu=" + self.Q, "--format=csv,noheader,nounits"],
-                    capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
-            except Exception:
-                pass
-            self.stop.wait(0.2)
+        self.proc = None
 
     def __enter__(self):
-        self.t.start()
+        # one nvidia-smi in loop mode (50 ms) for the whole timed region
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let the first sample land before timing
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self.stop.set()
-        self.t.join(timeout=10)
+        if self.proc is None:
+            return
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=10)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        for line in out.splitlines():
+            if line.strip():
+                self.samples.append([s.strip() for s in line.split(",")])
 
     def summary(self):
         if not self.samples:
@@ -168,7 +172,7 @@ def run_reference(args):
     if rank != 0:
         return
     k, n = args.k, args.n
-    n_sample = args.cpu_n
+    n_sample = args.cpu_n or n
     res = []
     for i in range(args.warmup + args.steps):
         r = cpu_baseline(k, n_sample)
@@ -286,7 +290,7 @@ def run_ours(args):
     overall_rate = wc["instr"] / (ms * 1e-3)
     cpu = None
     if not args.no_cpu and world == 1:
-        cpu = cpu_baseline(k, args.cpu_n)
+        cpu = cpu_baseline(k, args.cpu_n or n)
     clocks = clk.summary()
     line = {
         "metric": "%s LU+solve eff. GFLOP/s ((2/3)n^3/s)" % NAMES[k],
@@ -457,7 +461,8 @@ def main():
     ap.add_argument("--dim", dest="n", type=int, default=None)
     ap.add_argument("--nb", type=int, default=0)
     ap.add_argument("--dist-nb", type=int, default=256)
-    ap.add_argument("--cpu-n", type=int, default=768)
+    ap.add_argument("--cpu-n", type=int, default=0,
+                    help="CPU baseline sample size (0: the workload n)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.config == 4:
