@@ -39,6 +39,8 @@ struct LuWork {
   int32_t *swap_list = nullptr;              // [64 cur][64 src][count]
   int G = 0;                                 // max CTAs of the panel launch
   void *graphs = nullptr;                    // host-side graph cache
+  cudaStream_t side = nullptr;   // high-priority stream: look-ahead panels
+  cudaEvent_t ev_next = nullptr, ev_panel = nullptr;
   unsigned long long *trace = nullptr;       // diagnostics: [G][32][8] ns
   int trace_J = -1;                          // panel to trace (-1: none)
   cudaError_t init(int sms);

@@ -200,11 +200,20 @@ cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block,
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  // the panel is the critical path: highest priority so its CTAs are
+  // dispatched ahead of a concurrently running trailing update's
+  static const int prio = [] {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    return hi;
+  }();
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributePriority;
+  attr[1].val.priority = prio;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
@@ -278,13 +287,29 @@ struct GraphCache {
 // LU of the m x ncols matrix A (ncols <= m): ncols == m is the square
 // factorisation; ncols < m factors a tall block (the distributed LU's
 // panel), pivoting over all m rows and exchanging rows inside the block.
+//
+// Look-ahead (HPL style): after panel P's exchanges and TRSM, the trailing
+// update is split into the next panel's columns ("next") and the rest.  The
+// next panel is factored on the high-priority side stream as soon as its
+// columns are updated, concurrently with the rest of panel P's update on
+// the main stream (disjoint columns); the main stream waits for it before
+// panel P+1's exchanges.  Per element the order of operations is unchanged.
 cudaError_t enqueue_lu(int k, int m, int ncols, MatView A, int32_t *d_swaps,
                        int nb, LuWork &ws, cudaStream_t s) {
   cudaError_t e;
+  const bool ahead = ws.side != nullptr &&
+                     std::getenv("MPCORE_NO_LOOKAHEAD") == nullptr;
   if ((e = lu_begin(ws, s)) != cudaSuccess) return e;
+  bool panel_pending = false;  // panel J was factored on the side stream
   for (int J = 0; J < ncols; J += nb) {
     const int w = min(nb, ncols - J);
-    if ((e = lu_panel(k, m, A, J, w, d_swaps, ws, s)) != cudaSuccess) return e;
+    if (panel_pending) {
+      if ((e = cudaStreamWaitEvent(s, ws.ev_panel, 0)) != cudaSuccess) return e;
+      panel_pending = false;
+    } else {
+      if ((e = lu_panel(k, m, A, J, w, d_swaps, ws, s)) != cudaSuccess)
+        return e;
+    }
     if ((e = lu_laswp(k, A, 0, J, J + w, ncols, ws.swap_list, ws.status,
                       s)) != cudaSuccess)
       return e;
@@ -295,11 +320,34 @@ cudaError_t enqueue_lu(int k, int m, int ncols, MatView A, int32_t *d_swaps,
         return e;
     }
     if (rest_c > 0 && rest_r > 0) {
-      if ((e = lu_update(k, rest_r, rest_c, w, sub(A, J + w, J),
-                         sub(A, J, J + w), sub(A, J + w, J + w), ws.status,
-                         s)) != cudaSuccess)
+      const int J2 = J + w, w2 = min(nb, ncols - J2);
+      int first = rest_c;  // columns updated before the rest
+      if (ahead) first = w2;
+      if ((e = lu_update(k, rest_r, first, w, sub(A, J2, J), sub(A, J, J2),
+                         sub(A, J2, J2), ws.status, s)) != cudaSuccess)
         return e;
+      if (ahead) {
+        // next panel on the side stream, overlapping the rest of the update
+        if ((e = cudaEventRecord(ws.ev_next, s)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(ws.side, ws.ev_next, 0)) != cudaSuccess)
+          return e;
+        if ((e = lu_panel(k, m, A, J2, w2, d_swaps, ws, ws.side)) !=
+            cudaSuccess)
+          return e;
+        if ((e = cudaEventRecord(ws.ev_panel, ws.side)) != cudaSuccess)
+          return e;
+        panel_pending = true;
+        if (rest_c > first) {
+          if ((e = lu_update(k, rest_r, rest_c - first, w, sub(A, J2, J),
+                             sub(A, J, J2 + first), sub(A, J2, J2 + first),
+                             ws.status, s)) != cudaSuccess)
+            return e;
+        }
+      }
     }
+  }
+  if (panel_pending) {  // cannot happen (the last panel has no successor)
+    if ((e = cudaStreamWaitEvent(s, ws.ev_panel, 0)) != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
@@ -327,6 +375,16 @@ cudaError_t LuWork::init(int sms) {
   cudaMemset(epoch, 0, sizeof(unsigned));
   cudaMemset(status, 0xFF, sizeof(int32_t));
   graphs = new GraphCache();
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  if ((e = cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi)) !=
+      cudaSuccess)
+    return e;
+  if ((e = cudaEventCreateWithFlags(&ev_next, cudaEventDisableTiming)) !=
+          cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming)) !=
+          cudaSuccess)
+    return e;
   return cudaDeviceSynchronize();
 }
 
