@@ -234,11 +234,22 @@ cudaError_t lu_update(int k, int M, int N, int w, MatView L21, MatView U12,
   if (M <= 0 || N <= 0 || w <= 0) return cudaSuccess;
   prof_begin(PROF_UPDATE, s);
   cudaError_t e = cudaErrorInvalidValue;
-  switch (k) {
-    case 2: e = launch<2, true, false>(M, N, w, L21, U12, A22, status, s); break;
-    case 3: e = launch<3, true, false>(M, N, w, L21, U12, A22, status, s); break;
-    case 4: e = launch<4, true, false>(M, N, w, L21, U12, A22, status, s); break;
-    default: break;
+  if (N <= 32) {
+    // the look-ahead's next-panel columns: a tall, narrow update on the
+    // critical path -- small tiles so it spreads over every SM
+    switch (k) {
+      case 2: e = launch_t<2, TileT<16, 32, 16, 1, 2, 2>, true, false>(M, N, w, L21, U12, A22, status, s); break;
+      case 3: e = launch_t<3, TileT<8, 32, 16, 1, 1, 2>, true, false>(M, N, w, L21, U12, A22, status, s); break;
+      case 4: e = launch_t<4, TileT<8, 32, 16, 1, 1, 2>, true, false>(M, N, w, L21, U12, A22, status, s); break;
+      default: break;
+    }
+  } else {
+    switch (k) {
+      case 2: e = launch<2, true, false>(M, N, w, L21, U12, A22, status, s); break;
+      case 3: e = launch<3, true, false>(M, N, w, L21, U12, A22, status, s); break;
+      case 4: e = launch<4, true, false>(M, N, w, L21, U12, A22, status, s); break;
+      default: break;
+    }
   }
   prof_end(PROF_UPDATE, s);
   return e;

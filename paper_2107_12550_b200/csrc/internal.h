@@ -30,19 +30,21 @@ bool prof_enabled();
 constexpr int LU_MAX_W = 32, LU_MAX_K = 4;
 constexpr int LU_CAND_WORDS = 16;                    // idx, mag(2), pivot(2K)
 constexpr int LU_ROW_WORDS = 2 * LU_MAX_W * LU_MAX_K;  // a panel row, 2/double
+constexpr int LU_SWAP_LIST = 4 * LU_MAX_W + 1;         // one composed list
 struct LuWork {
   unsigned long long *cand_words = nullptr;  // [2][G][LU_CAND_WORDS]
   unsigned long long *row_words = nullptr;   // [2][G][LU_ROW_WORDS]
   unsigned long long *rowj_words = nullptr;  // [2][LU_ROW_WORDS]
   unsigned *epoch = nullptr;                 // [1] device LU call counter
   int32_t *status = nullptr;                 // [0] singular step (or -1)
-  int32_t *swap_list = nullptr;              // [64 cur][64 src][count]
+  int32_t *swap_list = nullptr;  // [2 slots][64 cur | 64 src | count]
   int G = 0;                                 // max CTAs of the panel launch
   void *graphs = nullptr;                    // host-side graph cache
   cudaStream_t side = nullptr;   // high-priority stream: look-ahead panels
   cudaEvent_t ev_next = nullptr, ev_panel = nullptr;
   unsigned long long *trace = nullptr;       // diagnostics: [G][32][8] ns
   int trace_J = -1;                          // panel to trace (-1: none)
+  unsigned poll_ns = 32;                     // back-off between polls
   cudaError_t init(int sms);
 };
 
@@ -92,8 +94,9 @@ cudaError_t lu_solve(int k, int n, MatView LU, const int32_t *d_perm,
 
 // panel pieces (exposed for the distributed driver)
 cudaError_t lu_begin(LuWork &ws, cudaStream_t s);
+// factor panel [J, J+w); its composed row exchanges go to swap-list slot
 cudaError_t lu_panel(int k, int n, MatView A, int J, int w, int32_t *d_swaps,
-                     LuWork &ws, cudaStream_t s);
+                     LuWork &ws, int slot, cudaStream_t s);
 // row exchanges of the last factored panel (composed in ws.swap_list by the
 // panel kernel) on columns [c0, c1) and [c2, c3)
 cudaError_t lu_laswp(int k, MatView A, int c0, int c1, int c2, int c3,

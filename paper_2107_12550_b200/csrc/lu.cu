@@ -224,7 +224,7 @@ size_t panel_smem(int R) {
 
 template <int K, int W>
 cudaError_t panel_k(int n, MatView A, int J, int w, int32_t *d_swaps,
-                    LuWork &ws, cudaStream_t s) {
+                    LuWork &ws, int slot, cudaStream_t s) {
   const int m = n - J;
   // Rows per CTA: the per-column candidate exchange costs ~0.6 us among 16
   // CTAs, ~0.9 us among 64 and ~1.9 us among 148 (tools/llbench.cu on
@@ -247,7 +247,7 @@ cudaError_t panel_k(int n, MatView A, int J, int w, int32_t *d_swaps,
     configured = smem;
   }
   return launch_coop(kern, dim3(G), dim3(PANEL_THREADS), smem, s, n, A, J, w,
-                     d_swaps, ws);
+                     d_swaps, ws, slot);
 }
 
 template <int K, int W>
@@ -258,6 +258,8 @@ cudaError_t trsm_k(MatView L11, MatView U12, int w, int ncols,
       L11, U12, w, ncols, status);
   return cudaGetLastError();
 }
+
+int madd_instr(int k) { return k == 2 ? 29 : k == 3 ? 214 : 326; }
 
 MatView sub(MatView A, int i, int j) {
   MatView v = A;
@@ -303,47 +305,79 @@ cudaError_t enqueue_lu(int k, int m, int ncols, MatView A, int32_t *d_swaps,
   bool panel_pending = false;  // panel J was factored on the side stream
   for (int J = 0; J < ncols; J += nb) {
     const int w = min(nb, ncols - J);
+    const int slot = (J / nb) & 1;
+    int32_t *sl = ws.swap_list + slot * LU_SWAP_LIST;
     if (panel_pending) {
       if ((e = cudaStreamWaitEvent(s, ws.ev_panel, 0)) != cudaSuccess) return e;
       panel_pending = false;
     } else {
-      if ((e = lu_panel(k, m, A, J, w, d_swaps, ws, s)) != cudaSuccess)
+      if ((e = lu_panel(k, m, A, J, w, d_swaps, ws, slot, s)) != cudaSuccess)
         return e;
     }
-    if ((e = lu_laswp(k, A, 0, J, J + w, ncols, ws.swap_list, ws.status,
-                      s)) != cudaSuccess)
-      return e;
     const int rest_r = m - J - w, rest_c = ncols - J - w;
-    if (rest_c > 0) {
-      if ((e = lu_trsm(k, sub(A, J, J), sub(A, J, J + w), w, rest_c,
+    const int J2 = J + w, w2 = min(nb, max(0, ncols - J2));
+    if (!ahead || rest_c <= 0 || rest_r <= 0) {
+      if ((e = lu_laswp(k, A, 0, J, J2, ncols, sl, ws.status, s)) !=
+          cudaSuccess)
+        return e;
+      if (rest_c > 0) {
+        if ((e = lu_trsm(k, sub(A, J, J), sub(A, J, J2), w, rest_c,
+                         ws.status, s)) != cudaSuccess)
+          return e;
+      }
+      if (rest_c > 0 && rest_r > 0) {
+        if ((e = lu_update(k, rest_r, rest_c, w, sub(A, J2, J), sub(A, J, J2),
+                           sub(A, J2, J2), ws.status, s)) != cudaSuccess)
+          return e;
+      }
+      continue;
+    }
+    // Where the rest of the update outlasts the next panel (early panels),
+    // exchanges and U12 run whole before the fork; near the end, where the
+    // panel chain is the critical path, only the next panel's columns do.
+    const double upd_s = (double)rest_r * rest_c * w * madd_instr(k) / 16e12;
+    static const bool split_on = std::getenv("MPCORE_LU_SPLIT") != nullptr;
+    const bool split = split_on && upd_s < 1.2 * (double)w2 * 4.5e-6;
+    const int c_first = split ? w2 : rest_c;  // columns prepared pre-fork
+    if (split) {
+      if ((e = lu_laswp(k, A, J2, J2 + w2, 0, 0, sl, ws.status, s)) !=
+          cudaSuccess)
+        return e;
+    } else {
+      if ((e = lu_laswp(k, A, 0, J, J2, ncols, sl, ws.status, s)) !=
+          cudaSuccess)
+        return e;
+    }
+    if ((e = lu_trsm(k, sub(A, J, J), sub(A, J, J2), w, c_first, ws.status,
+                     s)) != cudaSuccess)
+      return e;
+    if ((e = lu_update(k, rest_r, w2, w, sub(A, J2, J), sub(A, J, J2),
+                       sub(A, J2, J2), ws.status, s)) != cudaSuccess)
+      return e;
+    // next panel on the side stream ...
+    if ((e = cudaEventRecord(ws.ev_next, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(ws.side, ws.ev_next, 0)) != cudaSuccess)
+      return e;
+    if ((e = lu_panel(k, m, A, J2, w2, d_swaps, ws, slot ^ 1, ws.side)) !=
+        cudaSuccess)
+      return e;
+    if ((e = cudaEventRecord(ws.ev_panel, ws.side)) != cudaSuccess) return e;
+    panel_pending = true;
+    // ... while this panel's exchanges, U12 and update finish elsewhere
+    if (split) {
+      if ((e = lu_laswp(k, A, 0, J, J2 + w2, ncols, sl, ws.status, s)) !=
+          cudaSuccess)
+        return e;
+    }
+    if (rest_c > w2) {
+      if (split &&
+          (e = lu_trsm(k, sub(A, J, J), sub(A, J, J2 + w2), w, rest_c - w2,
                        ws.status, s)) != cudaSuccess)
         return e;
-    }
-    if (rest_c > 0 && rest_r > 0) {
-      const int J2 = J + w, w2 = min(nb, ncols - J2);
-      int first = rest_c;  // columns updated before the rest
-      if (ahead) first = w2;
-      if ((e = lu_update(k, rest_r, first, w, sub(A, J2, J), sub(A, J, J2),
-                         sub(A, J2, J2), ws.status, s)) != cudaSuccess)
+      if ((e = lu_update(k, rest_r, rest_c - w2, w, sub(A, J2, J),
+                         sub(A, J, J2 + w2), sub(A, J2, J2 + w2), ws.status,
+                         s)) != cudaSuccess)
         return e;
-      if (ahead) {
-        // next panel on the side stream, overlapping the rest of the update
-        if ((e = cudaEventRecord(ws.ev_next, s)) != cudaSuccess) return e;
-        if ((e = cudaStreamWaitEvent(ws.side, ws.ev_next, 0)) != cudaSuccess)
-          return e;
-        if ((e = lu_panel(k, m, A, J2, w2, d_swaps, ws, ws.side)) !=
-            cudaSuccess)
-          return e;
-        if ((e = cudaEventRecord(ws.ev_panel, ws.side)) != cudaSuccess)
-          return e;
-        panel_pending = true;
-        if (rest_c > first) {
-          if ((e = lu_update(k, rest_r, rest_c - first, w, sub(A, J2, J),
-                             sub(A, J, J2 + first), sub(A, J2, J2 + first),
-                             ws.status, s)) != cudaSuccess)
-            return e;
-        }
-      }
     }
   }
   if (panel_pending) {  // cannot happen (the last panel has no successor)
@@ -365,16 +399,17 @@ cudaError_t LuWork::init(int sms) {
   if ((e = cudaMalloc(&rowj_words, jw)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&epoch, sizeof(unsigned))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&status, sizeof(int32_t))) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&swap_list, (4 * LU_MAX_W + 1) * sizeof(int32_t))) !=
+  if ((e = cudaMalloc(&swap_list, 2 * LU_SWAP_LIST * sizeof(int32_t))) !=
       cudaSuccess)
     return e;
-  cudaMemset(swap_list, 0, (4 * LU_MAX_W + 1) * sizeof(int32_t));
+  cudaMemset(swap_list, 0, 2 * LU_SWAP_LIST * sizeof(int32_t));
   cudaMemset(cand_words, 0, cw);
   cudaMemset(row_words, 0, rwb);
   cudaMemset(rowj_words, 0, jw);
   cudaMemset(epoch, 0, sizeof(unsigned));
   cudaMemset(status, 0xFF, sizeof(int32_t));
   graphs = new GraphCache();
+  if (const char *pn = std::getenv("MPCORE_POLL_NS")) poll_ns = std::atoi(pn);
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   if ((e = cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi)) !=
@@ -394,20 +429,20 @@ cudaError_t lu_begin(LuWork &ws, cudaStream_t s) {
 }
 
 cudaError_t lu_panel(int k, int n, MatView A, int J, int w, int32_t *d_swaps,
-                     LuWork &ws, cudaStream_t s) {
+                     LuWork &ws, int slot, cudaStream_t s) {
   prof_begin(PROF_PANEL, s);
   cudaError_t e = cudaErrorInvalidValue;
   if (w <= 16) {
     switch (k) {
-      case 2: e = panel_k<2, 16>(n, A, J, w, d_swaps, ws, s); break;
-      case 3: e = panel_k<3, 16>(n, A, J, w, d_swaps, ws, s); break;
-      case 4: e = panel_k<4, 16>(n, A, J, w, d_swaps, ws, s); break;
+      case 2: e = panel_k<2, 16>(n, A, J, w, d_swaps, ws, slot, s); break;
+      case 3: e = panel_k<3, 16>(n, A, J, w, d_swaps, ws, slot, s); break;
+      case 4: e = panel_k<4, 16>(n, A, J, w, d_swaps, ws, slot, s); break;
     }
   } else if (w <= 32) {
     switch (k) {
-      case 2: e = panel_k<2, 32>(n, A, J, w, d_swaps, ws, s); break;
-      case 3: e = panel_k<3, 32>(n, A, J, w, d_swaps, ws, s); break;
-      case 4: e = panel_k<4, 32>(n, A, J, w, d_swaps, ws, s); break;
+      case 2: e = panel_k<2, 32>(n, A, J, w, d_swaps, ws, slot, s); break;
+      case 3: e = panel_k<3, 32>(n, A, J, w, d_swaps, ws, slot, s); break;
+      case 4: e = panel_k<4, 32>(n, A, J, w, d_swaps, ws, slot, s); break;
     }
   }
   prof_end(PROF_PANEL, s);

@@ -73,7 +73,7 @@ struct PanelSmem {
 template <int K, int W>
 __global__ void __launch_bounds__(PANEL_THREADS, 1)
 panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
-             LuWork ws) {
+             LuWork ws, int slot) {
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31;
   if (ws.status[0] >= 0) return;
@@ -159,10 +159,10 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       ws.trace[((int64_t)g * 32 + jj) * 8 + slot] = t;
     }
   };
-  auto poll = [](const u64 *p, unsigned seq) -> unsigned {
+  auto poll = [&](const u64 *p, unsigned seq) -> unsigned {
     u64 v = ld_volatile(p);
     while ((unsigned)v != seq) {
-      __nanosleep(POLL_NS);
+      __nanosleep(ws.poll_ns);
       v = ld_volatile(p);
     }
     return (unsigned)(v >> 32);
@@ -210,7 +210,7 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
           }
         }
         if (__all_sync(0xffffffffu, done == (1u << SPL) - 1u)) break;
-        __nanosleep(POLL_NS);
+        __nanosleep(ws.poll_ns);
       }
       double bm = -1.0;
       int br = INT_MAX;
@@ -387,11 +387,12 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       if (lane == (ia & 31)) { if (ia < 32) es0 = sb; else es1 = sb; }
       if (lane == (ib & 31)) { if (ib < 32) es0 = sa; else es1 = sa; }
     }
-    if (lane < cnt) { ws.swap_list[lane] = ec0; ws.swap_list[64 + lane] = es0; }
+    int32_t *sl = ws.swap_list + slot * LU_SWAP_LIST;
+    if (lane < cnt) { sl[lane] = ec0; sl[64 + lane] = es0; }
     if (lane + 32 < cnt) {
-      ws.swap_list[lane + 32] = ec1;
-      ws.swap_list[64 + lane + 32] = es1;
+      sl[lane + 32] = ec1;
+      sl[64 + lane + 32] = es1;
     }
-    if (lane == 0) ws.swap_list[128] = cnt;
+    if (lane == 0) sl[128] = cnt;
   }
 }
