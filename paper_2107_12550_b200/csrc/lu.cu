@@ -222,6 +222,22 @@ size_t panel_smem(int R) {
   return ((size_t)R * W * K + W * K) * sizeof(double);
 }
 
+template <int K, int W, int SPL>
+cudaError_t panel_launch(int G, size_t smem, int n, MatView A, int J, int w,
+                         int32_t *d_swaps, LuWork &ws, int slot,
+                         cudaStream_t s) {
+  auto kern = panel_kernel<K, W, SPL>;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(
+        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  return launch_coop(kern, dim3(G), dim3(PANEL_THREADS), smem, s, n, A, J, w,
+                     d_swaps, ws, slot);
+}
+
 template <int K, int W>
 cudaError_t panel_k(int n, MatView A, int J, int w, int32_t *d_swaps,
                     LuWork &ws, int slot, cudaStream_t s) {
@@ -238,16 +254,11 @@ cudaError_t panel_k(int n, MatView A, int J, int w, int32_t *d_swaps,
   int G = min(ws.G, max(1, (m + rows_target - 1) / rows_target));
   const int R = (m + G - 1) / G;
   size_t smem = panel_smem<K, W>(R);
-  auto kern = panel_kernel<K, W>;
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(
-        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
-  return launch_coop(kern, dim3(G), dim3(PANEL_THREADS), smem, s, n, A, J, w,
-                     d_swaps, ws, slot);
+  // the poll keeps every slot's words in registers: size it to G so the
+  // panel leaves room for update CTAs on its SMs (look-ahead overlap)
+  if (G <= 64)
+    return panel_launch<K, W, 2>(G, smem, n, A, J, w, d_swaps, ws, slot, s);
+  return panel_launch<K, W, 5>(G, smem, n, A, J, w, d_swaps, ws, slot, s);
 }
 
 template <int K, int W>

@@ -70,7 +70,7 @@ struct PanelSmem {
   int piv[LU_MAX_W];                 // winner of every column of the panel
 };
 
-template <int K, int W>
+template <int K, int W, int SPL>
 __global__ void __launch_bounds__(PANEL_THREADS, 1)
 panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
              LuWork ws, int slot) {
@@ -119,12 +119,11 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
     u64 *wd = ws.cand_words + ((int64_t)(jj & 1) * G + g) * LU_CAND_WORDS;
     if (lane == 0) {
       S.cand_row = br;
-      st_volatile(wd + 0, ll_word((unsigned)br, seq));
-      st_volatile(wd + 1, ll_word(lo32(bm), seq));
-      st_volatile(wd + 2, ll_word(hi32(bm), seq));
-    } else if (lane <= 2 * K && br != INT_MAX) {
-      const double v = at(br - rbeg, jj)[(lane - 1) >> 1];
-      st_volatile(wd + 2 + lane, ll_word((lane & 1) ? lo32(v) : hi32(v), seq));
+      st_volatile(wd, ll_word((unsigned)br, seq));
+    } else if (lane <= 2 * K) {
+      // the candidate's value (its |head| is the magnitude): 2K words
+      const double v = br != INT_MAX ? at(br - rbeg, jj)[(lane - 1) >> 1] : 0.0;
+      st_volatile(wd + lane, ll_word((lane & 1) ? lo32(v) : hi32(v), seq));
     }
   };
   // H: publish the candidate row of column jj (+ row J+jj if owned)
@@ -179,11 +178,10 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       const int j = J + jj, par = jj & 1;
       const unsigned seq = seq0 + jj;
       trace(jj, 0);
-      // every slot's index and |head| (the winner's pivot value is read
-      // afterwards: polling it from every slot costs more in L2 traffic
-      // than the extra, already-landed, round trip)
-      constexpr int SPL = 5;        // slots per lane (G <= 160)
-      constexpr int NW = 3;         // words per slot polled here
+      // every slot's row and value words (1 + 2K); the magnitude is the
+      // value's |head|, so the winner's pivot arrives with the poll itself
+      // SPL slots per lane (G <= 32 * SPL)
+      constexpr int NW = 1 + 2 * K;
       u64 wv[SPL][NW];
       unsigned done = 0;  // bit q: slot lane+32q complete (or absent)
 #pragma unroll
@@ -202,11 +200,11 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
 #pragma unroll
         for (int q = 0; q < SPL; ++q) {
           if (!(done & (1u << q))) {
-            bool head = true;
+            bool all = true;
 #pragma unroll
-            for (int x = 0; x < 3; ++x)
-              if ((unsigned)wv[q][x] != seq) head = false;
-            if (head) done |= 1u << q;
+            for (int x = 0; x < NW; ++x)
+              if ((unsigned)wv[q][x] != seq) all = false;
+            if (all) done |= 1u << q;
           }
         }
         if (__all_sync(0xffffffffu, done == (1u << SPL) - 1u)) break;
@@ -214,13 +212,21 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       }
       double bm = -1.0;
       int br = INT_MAX;
+      unsigned bw[2 * K];
+#pragma unroll
+      for (int x = 0; x < 2 * K; ++x) bw[x] = 0u;
 #pragma unroll
       for (int q = 0; q < SPL; ++q) {
         if (lane + 32 * q < G) {
-          int rr = (int)(wv[q][0] >> 32);
-          double mm = __longlong_as_double(
-              (long long)((wv[q][2] & 0xffffffff00000000ull) | (wv[q][1] >> 32)));
-          if (better(mm, rr, bm, br)) { bm = mm; br = rr; }
+          const int rr = (int)(wv[q][0] >> 32);
+          const double mm = fabs(__longlong_as_double(
+              (long long)((wv[q][2] & 0xffffffff00000000ull) | (wv[q][1] >> 32))));
+          if (rr != INT_MAX && better(mm, rr, bm, br)) {
+            bm = mm;
+            br = rr;
+#pragma unroll
+            for (int x = 0; x < 2 * K; ++x) bw[x] = (unsigned)(wv[q][1 + x] >> 32);
+          }
         }
       }
       double gm;
@@ -229,14 +235,13 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       trace(jj, 1);
       const int gw = (r - J) / R;
       if (g == 0 && lane == 0) swaps[j] = r;
-      // pivot value of the winner: lanes 0..2K-1 read its words
-      const u64 *pw = ws.cand_words + ((int64_t)par * G + gw) * LU_CAND_WORDS;
-      unsigned half = lane < 2 * K ? poll(pw + 3 + lane, seq) : 0u;
+      // pivot value of the winner: from the lane whose best slot won
+      const int src = __ffs(__ballot_sync(0xffffffffu, br == r)) - 1;
       double pv[K];
 #pragma unroll
       for (int c = 0; c < K; ++c) {
-        unsigned l = __shfl_sync(0xffffffffu, half, 2 * c);
-        unsigned h = __shfl_sync(0xffffffffu, half, 2 * c + 1);
+        unsigned l = __shfl_sync(0xffffffffu, bw[2 * c], src);
+        unsigned h = __shfl_sync(0xffffffffu, bw[2 * c + 1], src);
         pv[c] = __longlong_as_double((long long)(((u64)h << 32) | l));
       }
       const bool singular = pv[0] == 0.0;

@@ -59,3 +59,26 @@ def test_dev_trsm_blocked_matches_oracle():
     M = torch.from_numpy(U).cuda()
     be.trsm(buf, w, M, 0, 0, ncols)
     assert M.cpu().numpy().tobytes() == Uo.tobytes()
+
+
+@pytest.mark.parametrize("k,m,w", [(2, 4100, 32), (3, 2200, 32),
+                                   (4, 4740, 64), (2, 9000, 48)])
+def test_tall_block_lu_matches_oracle(k, m, w):
+    # tall blocks spread the panel over > 64 CTAs (the 5-slot poll path, up
+    # to one CTA per SM); w > 32 exercises the inner panel blocking
+    import ctypes
+    A = gen.planes(k, (m, w), 0, m, 4242 + m)
+    ref = A.copy()
+    sw_ref = np.zeros(w, dtype=np.int32)
+    step = np.zeros(1, dtype=np.int32)
+    I32 = ctypes.POINTER(ctypes.c_int32)
+    F = ctypes.POINTER(ctypes.c_double)
+    st = oracle.lib().mcref_lu_block(k, m, w, ref.ctypes.data_as(F), w, m * w,
+                                     sw_ref.ctypes.data_as(I32),
+                                     step.ctypes.data_as(I32))
+    assert st == 0 and step[0] == -1
+    be = DeviceBackend(k)
+    M = torch.from_numpy(A).cuda()
+    sw = be.lu_block(M, 0, 0, w)
+    assert sw.tobytes() == sw_ref.tobytes()
+    assert M.cpu().numpy().tobytes() == ref.tobytes()
