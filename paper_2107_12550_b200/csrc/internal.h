@@ -78,13 +78,14 @@ cudaError_t gemm(int k, bool neg_a, bool zero_init, int M, int N, int KK,
 // singular step or -1.  nb = panel width (<= 32).
 cudaError_t lu_factor(int k, int m, int ncols, MatView A, int32_t *d_swaps,
                       int nb, LuWork &w, int32_t *sing_step, cudaStream_t s);
-// Flags for the pipelined triangular solves (epoch-tagged, per block).
+// Scratch of the pipelined triangular solves: every final x_i is published
+// as 2K self-validating words (32-bit payload | 32-bit sequence), [2K][rows].
 struct SolveWork {
-  int *flags = nullptr;
-  int cap = 0;
-  int epoch = 0;
-  cudaError_t ensure(int nblk);
-  int next_epoch() { return ++epoch; }
+  unsigned long long *words = nullptr;
+  int64_t cap = 0;           // rows
+  unsigned seq = 0;
+  cudaError_t ensure(int64_t rows);
+  unsigned next_seq() { return ++seq; }
 };
 // x <- solve(LU, perm, b): x[i] = b[perm[i]] (the reference's swaps,
 // composed), then forward and back substitution.  b and x must not alias.

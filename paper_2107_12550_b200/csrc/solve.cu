@@ -5,17 +5,25 @@
 //       x_i = add(x_i, mul(-L_ij, x_j))            i > j      (504-509)
 //   backward, j descending:
 //       x_j = div(x_j, U_jj);  x_i = add(x_i, mul(U_ij, -x_j))   i < j (510-520)
-// Each x_i's chain keeps the reference's order (ascending j forward,
-// descending j backward).
+// Every x_i's chain keeps the reference's order (ascending j forward,
+// descending j backward); madd = add(acc, mul(a, b)), so a product may be
+// formed by another thread ahead of time and added in order.
 //
-// Parallel structure: rows are cut into blocks of RB; one CTA thread owns
-// one row and runs its chain in registers.  Columns are consumed in tiles of
-// CB: a tile of x becomes readable as soon as the CB rows it covers are
-// final (per-tile flag, epoch-tagged), so the next block starts on a tile
-// while the producing block is still resolving later rows of its diagonal
-// triangle.  L/U tiles are staged through shared memory with coalesced,
-// double-buffered cp.async loads.  CTAs are persistent (cooperative launch
-// => co-resident) and take blocks in dependency order.
+// Parallel structure.  Rows are cut into blocks of 32; a CTA (persistent,
+// cooperative => co-resident) takes blocks in dependency order.  In a CTA:
+//   warp 0, the owner: lane = row, the row's accumulator in registers.  It
+//     adds the products of every completed source block in order, runs the
+//     critical source block (the neighbour still being solved) with full
+//     madds as its x values appear, then the diagonal triangle with the
+//     x_j broadcast by shuffles (no CTA barrier on the per-row chain);
+//   warps 1-3, producers: for each completed source block, products
+//     P[r][c] = mul(-L_rc, x_c) (coalesced: lane = column) into a
+//     double-buffered shared-memory ring (named barriers FULL/EMPTY), and
+//     the L tiles of the critical source block and of the diagonal.
+// Products cost ~60 % of a madd (TD: 133 of 214 FP64 instructions), so the
+// owner's per-row chain is only the adds.  Every final x_i is published as
+// 2K self-validating 8-byte words (payload | sequence), so a consumer needs
+// no flag, no fence and a single L2 round trip per chunk of rows.
 #include "internal.h"
 #include "mc.cuh"
 
@@ -23,61 +31,62 @@ namespace mpk {
 
 namespace {
 
-constexpr int RB = 128;  // rows per block (= threads per CTA)
-constexpr int CB = 16;   // columns per staged tile (= rows per flag)
+constexpr int SB = 32;         // rows per block (owner lanes)
+constexpr int CH = 8;          // critical-block rows fetched per round trip
+constexpr int NPW = 3;         // producer warps
+constexpr int ST = 32 * (1 + NPW);
+constexpr int PS = SB + 1;     // padded row stride of the shared tiles
+constexpr int NSLOT = 2;
+constexpr int BAR_FULL = 1, BAR_EMPTY = 3, BAR_STAGED = 5;
 
-__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s),
-               "l"(gmem));
-}
-__device__ __forceinline__ void cp_commit() {
-  asm volatile("cp.async.commit_group;\n" ::);
-}
-template <int N> __device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
+using u64 = unsigned long long;
 
-__device__ __forceinline__ void wait_flag(const int *flags, int t,
-                                          int epoch) {
-  if (threadIdx.x == 0) {
-    const volatile int *f = flags + t;
-    while (*f < epoch) __nanosleep(20);
-    __threadfence();
-  }
-  __syncthreads();
+__device__ __forceinline__ void st_word(u64 *p, u64 v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v)
+               : "memory");
 }
-
-// the x rows of tile t are final: make them visible, then raise its flag
-__device__ __forceinline__ void publish(int *flags, int t, int epoch) {
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) atomicExch(flags + t, epoch);
+__device__ __forceinline__ u64 ld_word(const u64 *p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void nb_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(ST) : "memory");
+}
+__device__ __forceinline__ void nb_arrive(int id) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(ST) : "memory");
 }
 
-// Stage rows [r0, r0+RB) x cols [c0, c0+cw) of M into Ts[c][r][CB+1]
-// (asynchronous; caller commits / waits)
+// x_i (K doubles) -> words [2c][i] = lo, [2c+1][i] = hi, each | seq
 template <int K>
-__device__ __forceinline__ void stage_tile(double *Ts, MatView M, int n,
-                                           int r0, int c0, int cw) {
-  for (int e = threadIdx.x; e < RB * CB; e += RB) {
-    int r = e / CB, cc = e % CB;
-    if (r0 + r < n && cc < cw) {
+__device__ __forceinline__ void publish_x(u64 *W, int64_t n, int i,
+                                          const double *v, unsigned seq) {
 #pragma unroll
-      for (int c = 0; c < K; ++c)
-        cp_async8(Ts + (c * RB + r) * (CB + 1) + cc,
-                  M.p + c * M.plane + (int64_t)(r0 + r) * M.ld + c0 + cc);
-    }
+  for (int c = 0; c < K; ++c) {
+    const u64 b = (u64)__double_as_longlong(v[c]);
+    st_word(W + (2 * c) * n + i, (b << 32) | seq);
+    st_word(W + (2 * c + 1) * n + i, (b & 0xffffffff00000000ull) | seq);
   }
 }
-
+// poll row i's words until all carry seq; returns the K doubles
 template <int K>
-__device__ __forceinline__ void stage_x(double *xs, const double *x, int n,
-                                        int c0, int cw) {
-  for (int e = threadIdx.x; e < cw * K; e += RB) {
-    int c = e / cw, cc = e % cw;
-    xs[c * CB + cc] = __ldcg(x + (int64_t)c * n + c0 + cc);
+__device__ __forceinline__ void fetch_x(const u64 *W, int64_t n, int i,
+                                        unsigned seq, double *v) {
+  u64 w[2 * K];
+  for (;;) {
+#pragma unroll
+    for (int x = 0; x < 2 * K; ++x) w[x] = ld_word(W + x * n + i);
+    bool ok = true;
+#pragma unroll
+    for (int x = 0; x < 2 * K; ++x) ok &= (unsigned)w[x] == seq;
+    if (ok) break;
+    __nanosleep(16);
   }
+#pragma unroll
+  for (int c = 0; c < K; ++c)
+    v[c] = __longlong_as_double(
+        (long long)((w[2 * c + 1] & 0xffffffff00000000ull) | (w[2 * c] >> 32)));
 }
 
 // xw[i] = b[perm[i]]  (the reference's in-order swaps, composed)
@@ -92,191 +101,180 @@ __global__ void permute_kernel(int n, const int32_t *__restrict__ perm,
   for (int c = 0; c < K; ++c) xw[(int64_t)c * n + i] = b[(int64_t)c * n + src];
 }
 
-constexpr int TILE_ELEMS = RB * (CB + 1);
+constexpr int TILE = SB * PS;  // one plane of a shared tile
 
-template <int K>
-__global__ void __launch_bounds__(RB)
-forward_kernel(int n, MatView LU, double *__restrict__ x, int *flags,
-               int epoch) {
+// One kernel for both sweeps (BACK = false: forward with unit L).
+template <int K, bool BACK>
+__global__ void __launch_bounds__(ST, 1)
+sweep_kernel(int n, MatView LU, double *__restrict__ x, u64 *__restrict__ W,
+             unsigned seq) {
   extern __shared__ double sm[];
-  double *Ls0 = sm;                          // [2][K][RB][CB+1]
-  double *xs = Ls0 + 2 * K * TILE_ELEMS;     // [K][CB]
-  double *xown = xs + K * CB;                // [K][RB]
-  const int nblk = (n + RB - 1) / RB;
-  const int tid = threadIdx.x;
-  for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-    const int r0 = blk * RB, i = r0 + tid;
-    const bool live = i < n;
-    const int rend = min(n, r0 + RB);
-    double acc[K];
-#pragma unroll
-    for (int c = 0; c < K; ++c) acc[c] = live ? x[(int64_t)c * n + i] : 0.0;
-    // off-diagonal tiles, ascending; L tiles prefetched one ahead
-    const int ntile = r0 / CB;
-    if (ntile > 0) {
-      stage_tile<K>(Ls0, LU, n, r0, 0, CB);
-      cp_commit();
-    }
-    for (int t = 0; t < ntile; ++t) {
-      double *Ls = Ls0 + (t & 1) * K * TILE_ELEMS;
-      if (t + 1 < ntile) {
-        stage_tile<K>(Ls0 + ((t + 1) & 1) * K * TILE_ELEMS, LU, n, r0,
-                      (t + 1) * CB, CB);
-        cp_commit();
-      }
-      wait_flag(flags, t, epoch);
-      stage_x<K>(xs, x, n, t * CB, CB);
-      if (t + 1 < ntile) cp_wait<1>(); else cp_wait<0>();
-      __syncthreads();
-      if (live) {
-#pragma unroll 1
-        for (int jj = 0; jj < CB; ++jj) {
-          double l[K], xj[K];
-#pragma unroll
-          for (int c = 0; c < K; ++c) {
-            l[c] = -Ls[(c * RB + tid) * (CB + 1) + jj];
-            xj[c] = xs[c * CB + jj];
-          }
-          mc::madd<K>(acc, l, xj);
-        }
-      }
-      __syncthreads();
-    }
-    // diagonal triangle, tile by tile; each finished tile is published
-    for (int c0 = r0; c0 < rend; c0 += CB) {
-      const int cw = min(CB, rend - c0);
-      stage_tile<K>(Ls0, LU, n, r0, c0, cw);
-      cp_commit();
-      cp_wait<0>();
-      __syncthreads();
-      for (int jj = 0; jj < cw; ++jj) {
-        const int j = c0 + jj;
-        if (i == j) {
-#pragma unroll
-          for (int c = 0; c < K; ++c) {
-            xown[c * RB + tid] = acc[c];
-            x[(int64_t)c * n + i] = acc[c];   // final
-          }
-        }
-        __syncthreads();
-        if (live && i > j) {
-          double l[K], xj[K];
-#pragma unroll
-          for (int c = 0; c < K; ++c) {
-            l[c] = -Ls0[(c * RB + tid) * (CB + 1) + jj];
-            xj[c] = xown[c * RB + (j - r0)];
-          }
-          mc::madd<K>(acc, l, xj);
-        }
-      }
-      publish(flags, c0 / CB, epoch);
-    }
-  }
-}
+  double *P = sm;                        // [NSLOT][K][SB][PS] products
+  double *Lc = P + NSLOT * K * TILE;     // [K][SB][PS] critical source tile
+  double *Ld = Lc + K * TILE;            // [K][SB][PS] diagonal tile
+  const int nblk = (n + SB - 1) / SB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t N = n;
 
-template <int K>
-__global__ void __launch_bounds__(RB)
-backward_kernel(int n, MatView LU, double *__restrict__ x, int *flags,
-                int epoch) {
-  extern __shared__ double sm[];
-  double *Us0 = sm;
-  double *xs = Us0 + 2 * K * TILE_ELEMS;
-  double *xown = xs + K * CB;                // [K][RB]: -x_j of own block
-  const int nblk = (n + RB - 1) / RB;
-  const int ntile_all = (n + CB - 1) / CB;
-  const int tid = threadIdx.x;
   for (int q = blockIdx.x; q < nblk; q += gridDim.x) {
-    const int blk = nblk - 1 - q;
-    const int r0 = blk * RB, i = r0 + tid;
-    const int rend = min(n, r0 + RB);
-    const bool live = i < n;
-    double acc[K];
+    const int blk = BACK ? nblk - 1 - q : q;
+    const int r0 = blk * SB;
+    const int rows = min(SB, n - r0);
+    // completed source blocks, in fold order, and the critical one
+    const int crit = BACK ? blk + 1 : blk - 1;
+    const bool has_crit = crit >= 0 && crit < nblk;
+    const int nfull = BACK ? max(0, nblk - blk - 2) : max(0, blk - 1);
+    auto src_of = [&](int t) { return BACK ? nblk - 1 - t : t; };
+    __syncthreads();  // the previous block's tiles are no longer read
+
+    if (warp > 0) {
+      // ============================================================ producers
+      const int pw = warp - 1;
+      // stage the critical source tile and the diagonal tile (lane = column)
+      for (int r = pw; r < rows; r += NPW) {
+        const int64_t row = (int64_t)(r0 + r) * LU.ld;
+        if (has_crit) {
+          const int c = crit * SB + lane;
+          if (c < n) {
 #pragma unroll
-    for (int c = 0; c < K; ++c) acc[c] = live ? x[(int64_t)c * n + i] : 0.0;
-    // off-diagonal tiles of later rows, descending (tile index from the top
-    // tile of the matrix down to the first tile after this block)
-    const int t_lo = (rend + CB - 1) / CB;     // first tile after the block
-    const int nt = ntile_all - t_lo;
-    auto tile_c0 = [&](int q2) { return (ntile_all - 1 - q2) * CB; };
-    if (nt > 0) {
-      int c0 = tile_c0(0);
-      stage_tile<K>(Us0, LU, n, r0, c0, min(CB, n - c0));
-      cp_commit();
-    }
-    for (int q2 = 0; q2 < nt; ++q2) {
-      const int c0 = tile_c0(q2), cw = min(CB, n - c0);
-      double *Us = Us0 + (q2 & 1) * K * TILE_ELEMS;
-      if (q2 + 1 < nt) {
-        int c1 = tile_c0(q2 + 1);
-        stage_tile<K>(Us0 + ((q2 + 1) & 1) * K * TILE_ELEMS, LU, n, r0, c1,
-                      min(CB, n - c1));
-        cp_commit();
-      }
-      wait_flag(flags, c0 / CB, epoch);
-      stage_x<K>(xs, x, n, c0, cw);
-      if (q2 + 1 < nt) cp_wait<1>(); else cp_wait<0>();
-      __syncthreads();
-      if (live) {
-#pragma unroll 1
-        for (int jj = cw - 1; jj >= 0; --jj) {
-          double u[K], nx[K];
-#pragma unroll
-          for (int c = 0; c < K; ++c) {
-            u[c] = Us[(c * RB + tid) * (CB + 1) + jj];
-            nx[c] = -xs[c * CB + jj];
-          }
-          mc::madd<K>(acc, u, nx);
-        }
-      }
-      __syncthreads();
-    }
-    // diagonal triangle, tiles from the bottom; j descending
-    const int last_tile = (rend - 1) / CB;
-    for (int tt = last_tile; tt >= r0 / CB; --tt) {
-      const int c0 = tt * CB, cw = min(CB, rend - c0);
-      stage_tile<K>(Us0, LU, n, r0, c0, cw);
-      cp_commit();
-      cp_wait<0>();
-      __syncthreads();
-      for (int jj = cw - 1; jj >= 0; --jj) {
-        const int j = c0 + jj;
-        if (i == j) {
-          double u[K], qv[K];
-#pragma unroll
-          for (int c = 0; c < K; ++c) u[c] = Us0[(c * RB + tid) * (CB + 1) + jj];
-          mc::div<K>(acc, u, qv);
-#pragma unroll
-          for (int c = 0; c < K; ++c) {
-            acc[c] = qv[c];
-            xown[c * RB + tid] = -qv[c];
-            x[(int64_t)c * n + i] = qv[c];    // final
+            for (int k = 0; k < K; ++k)
+              Lc[k * TILE + r * PS + lane] = LU.p[k * LU.plane + row + c];
           }
         }
-        __syncthreads();
-        if (live && i < j) {
-          double u[K], nx[K];
+        if (r0 + lane < n) {
 #pragma unroll
-          for (int c = 0; c < K; ++c) {
-            u[c] = Us0[(c * RB + tid) * (CB + 1) + jj];
-            nx[c] = xown[c * RB + (j - r0)];
-          }
-          mc::madd<K>(acc, u, nx);
+          for (int k = 0; k < K; ++k)
+            Ld[k * TILE + r * PS + lane] = LU.p[k * LU.plane + row + r0 + lane];
         }
       }
-      publish(flags, tt, epoch);
+      nb_arrive(BAR_STAGED);
+      for (int t = 0; t < nfull; ++t) {
+        const int s = t & 1;
+        const int sb = src_of(t), c = sb * SB + lane;
+        if (t >= NSLOT) nb_sync(BAR_EMPTY + s);
+        if (c < n) {
+          double xv[K];
+          fetch_x<K>(W, N, c, seq, xv);
+          if (BACK) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) xv[k] = -xv[k];
+          }
+          double *Ps = P + s * K * TILE;
+          for (int r = pw; r < rows; r += NPW) {
+            double a[K], o[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              const double v = LU.p[k * LU.plane + (int64_t)(r0 + r) * LU.ld + c];
+              a[k] = BACK ? v : -v;
+            }
+            mc::mul<K>(a, xv, o);   // forward mul(-L, x); backward mul(U, -x)
+#pragma unroll
+            for (int k = 0; k < K; ++k) Ps[k * TILE + r * PS + lane] = o[k];
+          }
+        }
+        nb_arrive(BAR_FULL + s);
+      }
+    } else {
+      // ================================================================ owner
+      const int i = r0 + lane;
+      const bool live = lane < rows;
+      double acc[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[k] = live ? x[k * N + i] : 0.0;
+      for (int t = 0; t < nfull; ++t) {
+        const int s = t & 1;
+        const int sb = src_of(t);
+        const int cols = min(SB, n - sb * SB);
+        nb_sync(BAR_FULL + s);
+        const double *Ps = P + s * K * TILE + lane * PS;
+        if (live) {
+          if (BACK) {
+            for (int c = cols - 1; c >= 0; --c) {
+              double p[K], o[K];
+#pragma unroll
+              for (int k = 0; k < K; ++k) p[k] = Ps[k * TILE + c];
+              mc::add<K>(acc, p, o);
+#pragma unroll
+              for (int k = 0; k < K; ++k) acc[k] = o[k];
+            }
+          } else {
+            for (int c = 0; c < cols; ++c) {
+              double p[K], o[K];
+#pragma unroll
+              for (int k = 0; k < K; ++k) p[k] = Ps[k * TILE + c];
+              mc::add<K>(acc, p, o);
+#pragma unroll
+              for (int k = 0; k < K; ++k) acc[k] = o[k];
+            }
+          }
+        }
+        __syncwarp();
+        if (t + NSLOT < nfull) nb_arrive(BAR_EMPTY + s);
+      }
+      nb_sync(BAR_STAGED);
+      // critical source block: full madds as its rows become final
+      if (has_crit) {
+        const int c0 = crit * SB, cols = min(SB, n - c0);
+        const int nch = (cols + CH - 1) / CH;
+        for (int h = 0; h < nch; ++h) {
+          const int ch = BACK ? nch - 1 - h : h;
+          const int cb = ch * CH, cw = min(CH, cols - cb);
+          double xv[K];
+          if (lane < cw) fetch_x<K>(W, N, c0 + cb + lane, seq, xv);
+          __syncwarp();
+          for (int e = 0; e < cw; ++e) {
+            const int cc = BACK ? cw - 1 - e : e;
+            double xj[K], a[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              const double v = __shfl_sync(0xffffffffu, xv[k], cc);
+              const double l = Lc[k * TILE + lane * PS + cb + cc];
+              xj[k] = BACK ? -v : v;
+              a[k] = BACK ? l : -l;
+            }
+            if (live) mc::madd<K>(acc, a, xj);
+          }
+        }
+      }
+      // diagonal triangle; each row is published the moment it is final
+      for (int e = 0; e < rows; ++e) {
+        const int jj = BACK ? rows - 1 - e : e;
+        if (lane == jj) {
+          if (BACK) {
+            double u[K], qv[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) u[k] = Ld[k * TILE + lane * PS + lane];
+            mc::div<K>(acc, u, qv);
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc[k] = qv[k];
+          }
+#pragma unroll
+          for (int k = 0; k < K; ++k) x[k * N + i] = acc[k];
+          publish_x<K>(W, N, i, acc, seq);
+        }
+        double xj[K], a[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const double v = __shfl_sync(0xffffffffu, acc[k], jj);
+          const double l = Ld[k * TILE + lane * PS + jj];
+          xj[k] = BACK ? -v : v;
+          a[k] = BACK ? l : -l;
+        }
+        if (live && (BACK ? lane < jj : lane > jj)) mc::madd<K>(acc, a, xj);
+      }
     }
   }
 }
 
 template <int K>
-size_t solve_smem() {
-  return ((size_t)2 * K * TILE_ELEMS + K * CB + K * RB) * sizeof(double);
+size_t sweep_smem() {
+  return (size_t)(NSLOT + 2) * K * TILE * sizeof(double);
 }
 
 template <typename F>
 int coop_grid(F kern, size_t smem, int want) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, RB, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, ST, smem);
   int cap = per_sm * num_sms();
   if (cap < 1) cap = 1;
   return want < cap ? want : cap;
@@ -287,7 +285,7 @@ cudaError_t launch_coop(void (*kern)(KArgs...), int grid, size_t smem,
                         cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(RB);
+  cfg.blockDim = dim3(ST);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -301,9 +299,9 @@ cudaError_t launch_coop(void (*kern)(KArgs...), int grid, size_t smem,
 template <int K>
 cudaError_t solve_k(int n, MatView LU, const int32_t *perm, const double *b,
                     double *x, SolveWork &sw, cudaStream_t s) {
-  const size_t smem = solve_smem<K>();
-  auto fk = forward_kernel<K>;
-  auto bk = backward_kernel<K>;
+  const size_t smem = sweep_smem<K>();
+  auto fk = sweep_kernel<K, false>;
+  auto bk = sweep_kernel<K, true>;
   static bool configured = false;
   cudaError_t e;
   if (!configured) {
@@ -317,34 +315,31 @@ cudaError_t solve_k(int n, MatView LU, const int32_t *perm, const double *b,
       return e;
     configured = true;
   }
-  const int nblk = (n + RB - 1) / RB;
-  const int ntile = (n + CB - 1) / CB;
-  if ((e = sw.ensure(ntile)) != cudaSuccess) return e;
+  const int nblk = (n + SB - 1) / SB;
+  if ((e = sw.ensure(n)) != cudaSuccess) return e;
   permute_kernel<K><<<(n + 255) / 256, 256, 0, s>>>(n, perm, b, x);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  int epoch = sw.next_epoch();
-  int *flags = sw.flags;
-  e = launch_coop(fk, coop_grid(fk, smem, nblk), smem, s, n, LU, x, flags,
-                  epoch);
+  e = launch_coop(fk, coop_grid(fk, smem, nblk), smem, s, n, LU, x, sw.words,
+                  sw.next_seq());
   if (e != cudaSuccess) return e;
-  int epoch2 = sw.next_epoch();
-  return launch_coop(bk, coop_grid(bk, smem, nblk), smem, s, n, LU, x, flags,
-                     epoch2);
+  return launch_coop(bk, coop_grid(bk, smem, nblk), smem, s, n, LU, x,
+                     sw.words, sw.next_seq());
 }
 
 }  // namespace
 
-cudaError_t SolveWork::ensure(int nflags) {
-  if (nflags <= cap) return cudaSuccess;
-  if (flags) cudaFree(flags);
-  flags = nullptr;
+cudaError_t SolveWork::ensure(int64_t rows) {
+  if (rows <= cap) return cudaSuccess;
+  if (words) cudaFree(words);
+  words = nullptr;
   cap = 0;
-  epoch = 0;
-  cudaError_t e = cudaMalloc(&flags, (size_t)nflags * sizeof(int));
+  const size_t bytes = (size_t)2 * LU_MAX_K * rows * sizeof(u64);
+  cudaError_t e = cudaMalloc(&words, bytes);
   if (e != cudaSuccess) return e;
-  e = cudaMemset(flags, 0, (size_t)nflags * sizeof(int));
+  // sequence 0 is never used, so zeroed words are never valid
+  e = cudaMemset(words, 0, bytes);
   if (e != cudaSuccess) return e;
-  cap = nflags;
+  cap = rows;
   return cudaSuccess;
 }
 
