@@ -205,6 +205,10 @@ int32_t mpcore_prof_read(double *ms, int64_t *launches, int32_t cap);
 /* diagnostics: per-CTA, per-column phase timestamps (ns) of the panel
  * selected by the MPCORE_TRACE_PANEL environment variable; [SMs][32][8] */
 int32_t mpcore_debug_panel_trace(uint64_t *out_ns, int64_t cap);
+/* diagnostics: owner timestamps (ns) of every row block of the last solve
+ * (MPCORE_TRACE_SOLVE set): [forward, backward][blocks][4] = start, completed
+ * source blocks added, critical source block done, diagonal done */
+int32_t mpcore_debug_solve_trace(uint64_t *out_ns, int64_t cap);
 /* FP64 issue-rate microbenchmark: DADD instructions per second */
 int32_t mpcore_fp64_peak(double *dadd_per_s, double *dfma_per_s);
 

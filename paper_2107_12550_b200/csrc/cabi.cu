@@ -988,6 +988,19 @@ int32_t mpcore_debug_panel_trace(uint64_t *out_ns, int64_t cap) {
   return MPCORE_OK;
 }
 
+int32_t mpcore_debug_solve_trace(uint64_t *out_ns, int64_t cap) {
+  DevLock L;
+  if (L.st) return L.st;
+  Device &D = device();
+  if (!D.sw.trace) return fail(MPCORE_INTERNAL, "MPCORE_TRACE_SOLVE not set");
+  if (!out_ns || cap < D.sw.trace_len) return MPCORE_BAD_DIMENSION;
+  cudaError_t e = cudaMemcpy(out_ns, D.sw.trace,
+                             D.sw.trace_len * sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "trace");
+  return MPCORE_OK;
+}
+
 int32_t mpcore_prof_read(double *ms, int64_t *launches, int32_t cap) {
   if (!ms || !launches || cap < mpk::PROF_NSLOTS) return MPCORE_BAD_DIMENSION;
   DevLock L;

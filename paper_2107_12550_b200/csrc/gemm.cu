@@ -152,54 +152,144 @@ struct TileT {
 };
 
 template <int K, class T, bool NEG_A, bool ZERO>
-cudaError_t launch_t(int M, int N, int KK, MatView A, MatView B, MatView C,
-                     const int32_t *status, cudaStream_t s) {
+struct Launcher {
   using Cfg = GemmCfg<K, T::BM, T::BN, T::BK, T::TM, T::TN>;
-  auto kern = gemm_kernel<K, T::BM, T::BN, T::BK, T::TM, T::TN, NEG_A, ZERO,
-                          T::MINB>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(
-        kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    if (e != cudaSuccess) return e;
-    configured = true;
+  static constexpr auto kern =
+      gemm_kernel<K, T::BM, T::BN, T::BK, T::TM, T::TN, NEG_A, ZERO, T::MINB>;
+  // resident CTAs per SM (0 if the shape cannot launch)
+  static int slots() {
+    static const int v = [] {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)Cfg::SMEM) != cudaSuccess)
+        return 0;
+      int per = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, Cfg::NT,
+                                                    Cfg::SMEM);
+      return per;
+    }();
+    return v;
   }
-  dim3 grid((N + T::BN - 1) / T::BN, (M + T::BM - 1) / T::BM);
-  kern<<<grid, Cfg::NT, Cfg::SMEM, s>>>(M, N, KK, A, B, C, status);
-  return cudaGetLastError();
+  static cudaError_t run(int M, int N, int KK, MatView A, MatView B, MatView C,
+                         const int32_t *status, cudaStream_t s) {
+    if (slots() <= 0) return cudaErrorInvalidConfiguration;
+    dim3 grid((N + T::BN - 1) / T::BN, (M + T::BM - 1) / T::BM);
+    kern<<<grid, Cfg::NT, Cfg::SMEM, s>>>(M, N, KK, A, B, C, status);
+    return cudaGetLastError();
+  }
+};
+
+// Candidate tiles per precision: (index, BM, BN, BK, TM, TN, min CTAs/SM),
+// 256 threads each.
+#define MPK_TILES_DD(X)                                                       \
+  X(0, 64, 64, 16, 4, 4, 2) X(1, 32, 64, 16, 2, 4, 2)                         \
+  X(2, 64, 32, 16, 4, 2, 2) X(3, 32, 32, 16, 2, 2, 2)                         \
+  X(4, 16, 32, 16, 1, 2, 2) X(5, 32, 32, 16, 2, 2, 3)
+#define MPK_TILES_XD(X)                                                       \
+  X(0, 32, 32, 16, 2, 2, 1) X(1, 32, 16, 16, 2, 1, 2)                         \
+  X(2, 16, 32, 16, 1, 2, 2) X(3, 16, 16, 16, 1, 1, 2)                         \
+  X(4, 8, 32, 16, 1, 1, 2) X(5, 32, 32, 16, 2, 2, 2)
+// Their FP64 issue efficiency at a many-wave update shape (M = N = 8192,
+// KK = 32; tools/tile_sweep.py on B200), which the wave-aware chooser
+// weighs against tile quantisation.
+constexpr double TILE_EFF[3][6] = {
+    {0.940, 0.924, 0.918, 0.902, 0.852, 0.910},   // DD
+    {0.987, 0.981, 0.981, 0.976, 0.965, 0.990},   // TD
+    {0.975, 0.984, 0.987, 0.984, 0.976, 0.998}};  // QD
+constexpr int NTILES = 6;
+
+struct TileInfo {
+  int bm, bn, slots;
+  double eff;
+};
+
+template <int K, bool NEG_A, bool ZERO>
+TileInfo tile_info(int idx) {
+#define MPK_INFO(I, BM, BN, BK, TM, TN, MB)                                  \
+  case I:                                                                    \
+    return {BM, BN,                                                          \
+            Launcher<K, TileT<BM, BN, BK, TM, TN, MB>, NEG_A, ZERO>::slots(), \
+            TILE_EFF[K - 2][I]};
+  if constexpr (K == 2) {
+    switch (idx) { MPK_TILES_DD(MPK_INFO) }
+  } else {
+    switch (idx) { MPK_TILES_XD(MPK_INFO) }
+  }
+#undef MPK_INFO
+  return {1, 1, 0, 1.0};
 }
 
-// Tile shapes per precision.  Variant 0 is the default; the others are
-// kept selectable (MPCORE_GEMM_VARIANT) for tuning sweeps on the B200.
-int gemm_variant() {
+template <int K, bool NEG_A, bool ZERO>
+cudaError_t launch_idx(int idx, int M, int N, int KK, MatView A, MatView B,
+                       MatView C, const int32_t *status, cudaStream_t s) {
+#define MPK_RUN(I, BM, BN, BK, TM, TN, MB)                                    \
+  case I:                                                                    \
+    return Launcher<K, TileT<BM, BN, BK, TM, TN, MB>, NEG_A, ZERO>::run(      \
+        M, N, KK, A, B, C, status, s);
+  if constexpr (K == 2) {
+    switch (idx) { MPK_TILES_DD(MPK_RUN) }
+  } else {
+    switch (idx) { MPK_TILES_XD(MPK_RUN) }
+  }
+#undef MPK_RUN
+  return cudaErrorInvalidValue;
+}
+
+// MPCORE_GEMM_TILE=i forces candidate i (tuning sweeps); -1 = choose
+int tile_override() {
   static const int v = [] {
-    const char *e = std::getenv("MPCORE_GEMM_VARIANT");
-    return e ? std::atoi(e) : 0;
+    const char *e = std::getenv("MPCORE_GEMM_TILE");
+    return e ? std::atoi(e) : -1;
   }();
   return v;
 }
 
+// Every CTA of a wave costs the same (same KK), so the time of an M x N
+// product is ~ ceil(tiles / resident slots) * tile area / efficiency; pick
+// the candidate minimising it (the trailing update shrinks every panel, so
+// a fixed tile wastes up to a wave per launch).
 template <int K, bool NEG_A, bool ZERO>
-cudaError_t launch(int M, int N, int KK, MatView A, MatView B, MatView C,
-                   const int32_t *status, cudaStream_t s) {
-  const int v = gemm_variant();
-  if constexpr (K == 2) {
-    switch (v) {
-      case 1: return launch_t<K, TileT<64, 64, 16, 4, 4, 1>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
-      case 2: return launch_t<K, TileT<128, 64, 8, 8, 4, 1>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
-      case 3: return launch_t<K, TileT<64, 64, 8, 4, 4, 1>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
-      case 4: return launch_t<K, TileT<32, 64, 16, 2, 4, 2>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
-      default: return launch_t<K, TileT<64, 64, 16, 4, 4, 2>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
-    }
-  } else {
-    switch (v) {
-      case 1: return launch_t<K, TileT<32, 32, 16, 2, 2, 2>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
-      case 2: return launch_t<K, TileT<64, 32, 16, 4, 2, 1>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
-      case 3: return launch_t<K, TileT<32, 32, 8, 2, 2, 1>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
-      case 4: return launch_t<K, TileT<32, 16, 16, 2, 1, 2>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
-      default: return launch_t<K, TileT<32, 32, 16, 2, 2, 1>, NEG_A, ZERO>(M, N, KK, A, B, C, status, s);
+int choose_tile(int M, int N, unsigned mask = 0x3fu) {
+  const int forced = tile_override();
+  if (forced >= 0 && forced < NTILES) return forced;
+  const int sms = num_sms();
+  int best = 0;
+  double best_cost = 1e300;
+  for (int i = 0; i < NTILES; ++i) {
+    if (!(mask >> i & 1u)) continue;
+    const TileInfo t = tile_info<K, NEG_A, ZERO>(i);
+    if (t.slots <= 0) continue;
+    const int64_t tiles =
+        (int64_t)((M + t.bm - 1) / t.bm) * ((N + t.bn - 1) / t.bn);
+    const int64_t slots = (int64_t)t.slots * sms;
+    const double waves = (double)((tiles + slots - 1) / slots);
+    const double cost = waves * t.bm * t.bn * t.slots / t.eff;
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best = i;
     }
   }
+  return best;
+}
+
+template <int K, bool NEG_A, bool ZERO>
+cudaError_t launch(int M, int N, int KK, MatView A, MatView B, MatView C,
+                   const int32_t *status, cudaStream_t s,
+                   unsigned mask = 0x3fu) {
+  return launch_idx<K, NEG_A, ZERO>(choose_tile<K, NEG_A, ZERO>(M, N, mask),
+                                    M, N, KK, A, B, C, status, s);
+}
+
+// Candidates for the LU trailing update, which shares the GPU with the
+// look-ahead panel: measured over whole LUs (tools/tile_mask.sh, n = 2048)
+// the short-lived tiles win -- 16 x 16 for TD/QD, everything but 64 x 64
+// for DD.  MPCORE_UPDATE_TILES=mask overrides.
+unsigned update_mask(int k) {
+  static const unsigned v = [] {
+    const char *e = std::getenv("MPCORE_UPDATE_TILES");
+    return e ? (unsigned)std::strtoul(e, nullptr, 0) : 0u;
+  }();
+  if (v) return v;
+  return k == 2 ? 0x3eu : 0x08u;
 }
 
 }  // namespace
@@ -234,22 +324,11 @@ cudaError_t lu_update(int k, int M, int N, int w, MatView L21, MatView U12,
   if (M <= 0 || N <= 0 || w <= 0) return cudaSuccess;
   prof_begin(PROF_UPDATE, s);
   cudaError_t e = cudaErrorInvalidValue;
-  if (N <= 32) {
-    // the look-ahead's next-panel columns: a tall, narrow update on the
-    // critical path -- small tiles so it spreads over every SM
-    switch (k) {
-      case 2: e = launch_t<2, TileT<16, 32, 16, 1, 2, 2>, true, false>(M, N, w, L21, U12, A22, status, s); break;
-      case 3: e = launch_t<3, TileT<8, 32, 16, 1, 1, 2>, true, false>(M, N, w, L21, U12, A22, status, s); break;
-      case 4: e = launch_t<4, TileT<8, 32, 16, 1, 1, 2>, true, false>(M, N, w, L21, U12, A22, status, s); break;
-      default: break;
-    }
-  } else {
-    switch (k) {
-      case 2: e = launch<2, true, false>(M, N, w, L21, U12, A22, status, s); break;
-      case 3: e = launch<3, true, false>(M, N, w, L21, U12, A22, status, s); break;
-      case 4: e = launch<4, true, false>(M, N, w, L21, U12, A22, status, s); break;
-      default: break;
-    }
+  switch (k) {
+    case 2: e = launch<2, true, false>(M, N, w, L21, U12, A22, status, s, update_mask(2)); break;
+    case 3: e = launch<3, true, false>(M, N, w, L21, U12, A22, status, s, update_mask(3)); break;
+    case 4: e = launch<4, true, false>(M, N, w, L21, U12, A22, status, s, update_mask(4)); break;
+    default: break;
   }
   prof_end(PROF_UPDATE, s);
   return e;

@@ -84,6 +84,8 @@ struct SolveWork {
   unsigned long long *words = nullptr;
   int64_t cap = 0;           // rows
   unsigned seq = 0;
+  unsigned long long *trace = nullptr;  // MPCORE_TRACE_SOLVE diagnostics
+  int64_t trace_len = 0;
   cudaError_t ensure(int64_t rows);
   unsigned next_seq() { return ++seq; }
 };

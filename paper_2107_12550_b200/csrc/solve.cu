@@ -24,6 +24,8 @@
 // owner's per-row chain is only the adds.  Every final x_i is published as
 // 2K self-validating 8-byte words (payload | sequence), so a consumer needs
 // no flag, no fence and a single L2 round trip per chunk of rows.
+#include <cstdlib>
+
 #include "internal.h"
 #include "mc.cuh"
 
@@ -107,7 +109,7 @@ constexpr int TILE = SB * PS;  // one plane of a shared tile
 template <int K, bool BACK>
 __global__ void __launch_bounds__(ST, 1)
 sweep_kernel(int n, MatView LU, double *__restrict__ x, u64 *__restrict__ W,
-             unsigned seq) {
+             unsigned seq, u64 *trace) {
   extern __shared__ double sm[];
   double *P = sm;                        // [NSLOT][K][SB][PS] products
   double *Lc = P + NSLOT * K * TILE;     // [K][SB][PS] critical source tile
@@ -176,6 +178,14 @@ sweep_kernel(int n, MatView LU, double *__restrict__ x, u64 *__restrict__ W,
       }
     } else {
       // ================================================================ owner
+      auto mark = [&](int slot) {
+        if (trace && lane == 0) {
+          u64 t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          trace[(int64_t)blk * 4 + slot] = t;
+        }
+      };
+      mark(0);
       const int i = r0 + lane;
       const bool live = lane < rows;
       double acc[K];
@@ -211,6 +221,7 @@ sweep_kernel(int n, MatView LU, double *__restrict__ x, u64 *__restrict__ W,
         __syncwarp();
         if (t + NSLOT < nfull) nb_arrive(BAR_EMPTY + s);
       }
+      mark(1);
       nb_sync(BAR_STAGED);
       // critical source block: full madds as its rows become final
       if (has_crit) {
@@ -236,6 +247,7 @@ sweep_kernel(int n, MatView LU, double *__restrict__ x, u64 *__restrict__ W,
           }
         }
       }
+      mark(2);
       // diagonal triangle; each row is published the moment it is final
       for (int e = 0; e < rows; ++e) {
         const int jj = BACK ? rows - 1 - e : e;
@@ -262,6 +274,7 @@ sweep_kernel(int n, MatView LU, double *__restrict__ x, u64 *__restrict__ W,
         }
         if (live && (BACK ? lane < jj : lane > jj)) mc::madd<K>(acc, a, xj);
       }
+      mark(3);
     }
   }
 }
@@ -319,11 +332,12 @@ cudaError_t solve_k(int n, MatView LU, const int32_t *perm, const double *b,
   if ((e = sw.ensure(n)) != cudaSuccess) return e;
   permute_kernel<K><<<(n + 255) / 256, 256, 0, s>>>(n, perm, b, x);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  u64 *tf = sw.trace, *tb = sw.trace ? sw.trace + (int64_t)4 * nblk : nullptr;
   e = launch_coop(fk, coop_grid(fk, smem, nblk), smem, s, n, LU, x, sw.words,
-                  sw.next_seq());
+                  sw.next_seq(), tf);
   if (e != cudaSuccess) return e;
   return launch_coop(bk, coop_grid(bk, smem, nblk), smem, s, n, LU, x,
-                     sw.words, sw.next_seq());
+                     sw.words, sw.next_seq(), tb);
 }
 
 }  // namespace
@@ -340,6 +354,13 @@ cudaError_t SolveWork::ensure(int64_t rows) {
   e = cudaMemset(words, 0, bytes);
   if (e != cudaSuccess) return e;
   cap = rows;
+  if (std::getenv("MPCORE_TRACE_SOLVE")) {
+    // diagnostics: [2 sweeps][blocks][4] globaltimer stamps of each owner
+    if (trace) cudaFree(trace);
+    trace_len = 2 * 4 * ((rows + SB - 1) / SB);
+    e = cudaMalloc(&trace, trace_len * sizeof(u64));
+    if (e != cudaSuccess) return e;
+  }
   return cudaSuccess;
 }
 
