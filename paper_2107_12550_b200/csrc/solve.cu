@@ -71,6 +71,24 @@ __device__ __forceinline__ void publish_x(u64 *W, int64_t n, int i,
     st_word(W + (2 * c + 1) * n + i, (b & 0xffffffff00000000ull) | seq);
   }
 }
+// publish_x under a predicate, without a branch (keeps the per-row chain of
+// the triangle free of divergent blocks)
+template <int K>
+__device__ __forceinline__ void publish_x_if(bool p, u64 *W, int64_t n, int i,
+                                             const double *v, unsigned seq) {
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    const u64 b = (u64)__double_as_longlong(v[c]);
+    const u64 lo = (b << 32) | seq, hi = (b & 0xffffffff00000000ull) | seq;
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t"
+        "@q st.relaxed.gpu.global.u64 [%1], %2;\n\t"
+        "@q st.relaxed.gpu.global.u64 [%3], %4;\n\t}" ::"r"((unsigned)p),
+        "l"(W + (2 * c) * n + i), "l"(lo), "l"(W + (2 * c + 1) * n + i),
+        "l"(hi)
+        : "memory");
+  }
+}
 // poll row i's words until all carry seq; returns the K doubles
 template <int K>
 __device__ __forceinline__ void fetch_x(const u64 *W, int64_t n, int i,
@@ -155,6 +173,21 @@ sweep_kernel(int n, MatView LU, double *__restrict__ x, u64 *__restrict__ W,
         const int sb = src_of(t), c = sb * SB + lane;
         if (t >= NSLOT) nb_sync(BAR_EMPTY + s);
         if (c < n) {
+          // the tile's L/U values do not depend on x: load them first, so
+          // their latency overlaps the wait for the source block's x
+          constexpr int RPW = (SB + NPW - 1) / NPW;
+          double lv[RPW][K];
+#pragma unroll
+          for (int q = 0; q < RPW; ++q) {
+            const int r = pw + q * NPW;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+              const double v =
+                  r < rows ? LU.p[k * LU.plane + (int64_t)(r0 + r) * LU.ld + c]
+                           : 0.0;
+              lv[q][k] = BACK ? v : -v;
+            }
+          }
           double xv[K];
           fetch_x<K>(W, N, c, seq, xv);
           if (BACK) {
@@ -162,16 +195,15 @@ sweep_kernel(int n, MatView LU, double *__restrict__ x, u64 *__restrict__ W,
             for (int k = 0; k < K; ++k) xv[k] = -xv[k];
           }
           double *Ps = P + s * K * TILE;
-          for (int r = pw; r < rows; r += NPW) {
-            double a[K], o[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-              const double v = LU.p[k * LU.plane + (int64_t)(r0 + r) * LU.ld + c];
-              a[k] = BACK ? v : -v;
+          for (int q = 0; q < RPW; ++q) {
+            const int r = pw + q * NPW;
+            if (r < rows) {
+              double o[K];
+              mc::mul<K>(lv[q], xv, o);  // fwd mul(-L, x); back mul(U, -x)
+#pragma unroll
+              for (int k = 0; k < K; ++k) Ps[k * TILE + r * PS + lane] = o[k];
             }
-            mc::mul<K>(a, xv, o);   // forward mul(-L, x); backward mul(U, -x)
-#pragma unroll
-            for (int k = 0; k < K; ++k) Ps[k * TILE + r * PS + lane] = o[k];
           }
         }
         nb_arrive(BAR_FULL + s);
@@ -182,7 +214,7 @@ sweep_kernel(int n, MatView LU, double *__restrict__ x, u64 *__restrict__ W,
         if (trace && lane == 0) {
           u64 t;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-          trace[(int64_t)blk * 4 + slot] = t;
+          trace[(int64_t)blk * 8 + slot] = t;
         }
       };
       mark(0);
@@ -223,56 +255,93 @@ sweep_kernel(int n, MatView LU, double *__restrict__ x, u64 *__restrict__ W,
       }
       mark(1);
       nb_sync(BAR_STAGED);
-      // critical source block: full madds as its rows become final
+      // critical source block: full madds as its rows become final.  Every
+      // lane polls its own row of the block; each poll brings in all rows
+      // published so far, and the ready ones are consumed in fold order.
       if (has_crit) {
         const int c0 = crit * SB, cols = min(SB, n - c0);
-        const int nch = (cols + CH - 1) / CH;
-        for (int h = 0; h < nch; ++h) {
-          const int ch = BACK ? nch - 1 - h : h;
-          const int cb = ch * CH, cw = min(CH, cols - cb);
-          double xv[K];
-          if (lane < cw) fetch_x<K>(W, N, c0 + cb + lane, seq, xv);
-          __syncwarp();
-          for (int e = 0; e < cw; ++e) {
-            const int cc = BACK ? cw - 1 - e : e;
-            double xj[K], a[K];
+        double xv[K];
+        bool have = lane >= cols;
+        unsigned ready = __ballot_sync(0xffffffffu, have);
+        int done = 0, iters = 0;
+        mark(4);
+        while (done < cols) {
+          ++iters;
+          // re-poll the missing rows; the loads fly while the ready
+          // columns are consumed
+          u64 w[2 * K];
+          const bool polled = !have;
+          if (polled) {
+#pragma unroll
+            for (int x = 0; x < 2 * K; ++x) w[x] = ld_word(W + x * N + c0 + lane);
+          }
+          for (; done < cols; ++done) {
+            const int cc = BACK ? cols - 1 - done : done;
+            if (!(ready >> cc & 1u)) break;
+            double xj[K], a[K], o[K];
 #pragma unroll
             for (int k = 0; k < K; ++k) {
               const double v = __shfl_sync(0xffffffffu, xv[k], cc);
-              const double l = Lc[k * TILE + lane * PS + cb + cc];
+              const double l = Lc[k * TILE + lane * PS + cc];
               xj[k] = BACK ? -v : v;
               a[k] = BACK ? l : -l;
+              o[k] = acc[k];
             }
-            if (live) mc::madd<K>(acc, a, xj);
+            mc::madd<K>(o, a, xj);
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc[k] = live ? o[k] : acc[k];
           }
+          if (polled) {
+            bool ok = true;
+#pragma unroll
+            for (int x = 0; x < 2 * K; ++x) ok &= (unsigned)w[x] == seq;
+            if (ok) {
+              have = true;
+#pragma unroll
+              for (int k = 0; k < K; ++k)
+                xv[k] = __longlong_as_double((long long)(
+                    (w[2 * k + 1] & 0xffffffff00000000ull) | (w[2 * k] >> 32)));
+            }
+          }
+          const unsigned prev = ready;
+          ready = __ballot_sync(0xffffffffu, have);
+          if (prev != ready && __popc(ready) == 32) mark(5);
+          if (iters == 1) mark(7);
         }
+        if (trace && lane == 0) trace[(int64_t)blk * 8 + 6] = iters;
       }
       mark(2);
       // diagonal triangle; each row is published the moment it is final
       for (int e = 0; e < rows; ++e) {
         const int jj = BACK ? rows - 1 - e : e;
-        if (lane == jj) {
-          if (BACK) {
-            double u[K], qv[K];
+        if (BACK && lane == jj) {
+          double u[K], qv[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) u[k] = Ld[k * TILE + lane * PS + lane];
-            mc::div<K>(acc, u, qv);
+          for (int k = 0; k < K; ++k) u[k] = Ld[k * TILE + lane * PS + lane];
+          mc::div<K>(acc, u, qv);
 #pragma unroll
-            for (int k = 0; k < K; ++k) acc[k] = qv[k];
-          }
-#pragma unroll
-          for (int k = 0; k < K; ++k) x[k * N + i] = acc[k];
+          for (int k = 0; k < K; ++k) acc[k] = qv[k];
           publish_x<K>(W, N, i, acc, seq);
         }
-        double xj[K], a[K];
+        double xj[K], a[K], o[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const double v = __shfl_sync(0xffffffffu, acc[k], jj);
           const double l = Ld[k * TILE + lane * PS + jj];
           xj[k] = BACK ? -v : v;
           a[k] = BACK ? l : -l;
+          o[k] = acc[k];
         }
-        if (live && (BACK ? lane < jj : lane > jj)) mc::madd<K>(acc, a, xj);
+        // forward: row jj is final; publish it (predicated, off the chain)
+        if (!BACK) publish_x_if<K>(lane == jj, W, N, i, acc, seq);
+        mc::madd<K>(o, a, xj);
+        const bool upd = live && (BACK ? lane < jj : lane > jj);
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] = upd ? o[k] : acc[k];
+      }
+      if (live) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) x[k * N + i] = acc[k];
       }
       mark(3);
     }
@@ -332,7 +401,7 @@ cudaError_t solve_k(int n, MatView LU, const int32_t *perm, const double *b,
   if ((e = sw.ensure(n)) != cudaSuccess) return e;
   permute_kernel<K><<<(n + 255) / 256, 256, 0, s>>>(n, perm, b, x);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  u64 *tf = sw.trace, *tb = sw.trace ? sw.trace + (int64_t)4 * nblk : nullptr;
+  u64 *tf = sw.trace, *tb = sw.trace ? sw.trace + (int64_t)8 * nblk : nullptr;
   e = launch_coop(fk, coop_grid(fk, smem, nblk), smem, s, n, LU, x, sw.words,
                   sw.next_seq(), tf);
   if (e != cudaSuccess) return e;
@@ -357,7 +426,7 @@ cudaError_t SolveWork::ensure(int64_t rows) {
   if (std::getenv("MPCORE_TRACE_SOLVE")) {
     // diagnostics: [2 sweeps][blocks][4] globaltimer stamps of each owner
     if (trace) cudaFree(trace);
-    trace_len = 2 * 4 * ((rows + SB - 1) / SB);
+    trace_len = 2 * 8 * ((rows + SB - 1) / SB);
     e = cudaMalloc(&trace, trace_len * sizeof(u64));
     if (e != cudaSuccess) return e;
   }
