@@ -192,6 +192,92 @@ trsm_kernel(MatView L11, MatView U12, int w, int ncols,
   }
 }
 
+// Row exchanges + U12 in one pass, one warp per column (lane = panel row):
+// every read of the column (the composed exchange sources and the post-
+// exchange panel rows) happens before any write, so the exchanges need no
+// second sweep; U12 = L11^-1 A12 runs in registers, x_t broadcast by
+// shuffles (no CTA barrier per step).  Columns [c2, c3) get both, [c0, c1)
+// (the already factored L columns) only the exchanges.
+template <int K>
+__global__ void __launch_bounds__(128)
+swap_trsm_kernel(MatView A, int J, int w, int c0, int c1, int c2, int c3,
+                 const int32_t *__restrict__ swap_list,
+                 const int32_t *__restrict__ status) {
+  if (status[0] >= 0) return;
+  __shared__ int cur[2 * LU_MAX_W], src[2 * LU_MAX_W], rsrc[LU_MAX_W];
+  __shared__ double Ls[K][LU_MAX_W][LU_MAX_W + 1];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nright = (c3 - c2 + 3) / 4;
+  const bool right = (int)blockIdx.x < nright;
+  const int col = right ? c2 + blockIdx.x * 4 + warp
+                        : c0 + (blockIdx.x - nright) * 4 + warp;
+  const int cend = right ? c3 : c1;
+  const int cnt = swap_list[4 * LU_MAX_W];
+  if (tid < 2 * LU_MAX_W) {
+    cur[tid] = swap_list[tid];
+    src[tid] = swap_list[2 * LU_MAX_W + tid];
+  }
+  if (right) {
+    for (int e = tid; e < w * w; e += 128) {
+      const int r = e / w, q = e % w;
+      if (q < r) {
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          Ls[k][r][q] = -A.p[k * A.plane + (int64_t)(J + r) * A.ld + J + q];
+      }
+    }
+  }
+  __syncthreads();
+  if (right && tid < w) {
+    int rs = J + tid;
+    for (int i = 0; i < cnt; ++i)
+      if (cur[i] == J + tid) rs = src[i];
+    rsrc[tid] = rs;
+  }
+  __syncthreads();
+  if (col >= cend) return;
+  const int64_t ld = A.ld;
+  double *pc = A.p + col;
+  // exchange entries (lane, lane + 32); with U12 the panel rows are written
+  // by the solve below, so only destinations below the panel are kept here
+  const int i0 = lane, i1 = lane + 32;
+  const bool e0 = i0 < cnt && (!right || cur[i0] >= J + w);
+  const bool e1 = i1 < cnt && (!right || cur[i1] >= J + w);
+  double v0[K], v1[K], u[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    v0[k] = e0 ? pc[k * A.plane + (int64_t)src[i0] * ld] : 0.0;
+    v1[k] = e1 ? pc[k * A.plane + (int64_t)src[i1] * ld] : 0.0;
+    u[k] = (right && lane < w) ? pc[k * A.plane + (int64_t)rsrc[lane] * ld]
+                               : 0.0;
+  }
+  __syncwarp();
+  if (right) {
+    for (int t = 0; t + 1 < w; ++t) {
+      double ut[K], l[K], o[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        ut[k] = __shfl_sync(0xffffffffu, u[k], t);
+        l[k] = Ls[k][lane][t];
+        o[k] = u[k];
+      }
+      mc::madd<K>(o, l, ut);
+      const bool upd = lane > t && lane < w;
+#pragma unroll
+      for (int k = 0; k < K; ++k) u[k] = upd ? o[k] : u[k];
+    }
+    if (lane < w) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) pc[k * A.plane + (int64_t)(J + lane) * ld] = u[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if (e0) pc[k * A.plane + (int64_t)cur[i0] * ld] = v0[k];
+    if (e1) pc[k * A.plane + (int64_t)cur[i1] * ld] = v1[k];
+  }
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block,
                         size_t smem, cudaStream_t s, Args... args) {
@@ -270,7 +356,6 @@ cudaError_t trsm_k(MatView L11, MatView U12, int w, int ncols,
   return cudaGetLastError();
 }
 
-int madd_instr(int k) { return k == 2 ? 29 : k == 3 ? 214 : 326; }
 
 MatView sub(MatView A, int i, int j) {
   MatView v = A;
@@ -296,6 +381,24 @@ struct GraphCache {
   };
   std::vector<Entry> entries;
 };
+
+// exchanges of the last panel (slot list) on [c0, c1) and, with U12, on
+// [c2, c3)
+cudaError_t lu_swap_trsm(int k, MatView A, int J, int w, int c0, int c1,
+                         int c2, int c3, const int32_t *swap_list,
+                         const int32_t *status, cudaStream_t s) {
+  const int nl = (max(0, c1 - c0) + 3) / 4, nr = (max(0, c3 - c2) + 3) / 4;
+  if (nl + nr == 0) return cudaSuccess;
+  prof_begin(PROF_TRSM, s);
+  switch (k) {
+    case 2: swap_trsm_kernel<2><<<nl + nr, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status); break;
+    case 3: swap_trsm_kernel<3><<<nl + nr, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status); break;
+    case 4: swap_trsm_kernel<4><<<nl + nr, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status); break;
+    default: return cudaErrorInvalidValue;
+  }
+  prof_end(PROF_TRSM, s);
+  return cudaGetLastError();
+}
 
 // LU of the m x ncols matrix A (ncols <= m): ncols == m is the square
 // factorisation; ncols < m factors a tall block (the distributed LU's
@@ -327,45 +430,22 @@ cudaError_t enqueue_lu(int k, int m, int ncols, MatView A, int32_t *d_swaps,
     }
     const int rest_r = m - J - w, rest_c = ncols - J - w;
     const int J2 = J + w, w2 = min(nb, max(0, ncols - J2));
-    if (!ahead || rest_c <= 0 || rest_r <= 0) {
-      if ((e = lu_laswp(k, A, 0, J, J2, ncols, sl, ws.status, s)) !=
-          cudaSuccess)
+    // exchanges on every other column, U12 of the trailing columns
+    if ((e = lu_swap_trsm(k, A, J, w, 0, J, J2, ncols, sl, ws.status, s)) !=
+        cudaSuccess)
+      return e;
+    if (rest_c <= 0 || rest_r <= 0) continue;
+    if (!ahead) {
+      if ((e = lu_update(k, rest_r, rest_c, w, sub(A, J2, J), sub(A, J, J2),
+                         sub(A, J2, J2), ws.status, s)) != cudaSuccess)
         return e;
-      if (rest_c > 0) {
-        if ((e = lu_trsm(k, sub(A, J, J), sub(A, J, J2), w, rest_c,
-                         ws.status, s)) != cudaSuccess)
-          return e;
-      }
-      if (rest_c > 0 && rest_r > 0) {
-        if ((e = lu_update(k, rest_r, rest_c, w, sub(A, J2, J), sub(A, J, J2),
-                           sub(A, J2, J2), ws.status, s)) != cudaSuccess)
-          return e;
-      }
       continue;
     }
-    // Where the rest of the update outlasts the next panel (early panels),
-    // exchanges and U12 run whole before the fork; near the end, where the
-    // panel chain is the critical path, only the next panel's columns do.
-    const double upd_s = (double)rest_r * rest_c * w * madd_instr(k) / 16e12;
-    static const bool split_on = std::getenv("MPCORE_LU_SPLIT") != nullptr;
-    const bool split = split_on && upd_s < 1.2 * (double)w2 * 4.5e-6;
-    const int c_first = split ? w2 : rest_c;  // columns prepared pre-fork
-    if (split) {
-      if ((e = lu_laswp(k, A, J2, J2 + w2, 0, 0, sl, ws.status, s)) !=
-          cudaSuccess)
-        return e;
-    } else {
-      if ((e = lu_laswp(k, A, 0, J, J2, ncols, sl, ws.status, s)) !=
-          cudaSuccess)
-        return e;
-    }
-    if ((e = lu_trsm(k, sub(A, J, J), sub(A, J, J2), w, c_first, ws.status,
-                     s)) != cudaSuccess)
-      return e;
+    // the next panel's columns first ...
     if ((e = lu_update(k, rest_r, w2, w, sub(A, J2, J), sub(A, J, J2),
                        sub(A, J2, J2), ws.status, s)) != cudaSuccess)
       return e;
-    // next panel on the side stream ...
+    // ... then the next panel on the side stream ...
     if ((e = cudaEventRecord(ws.ev_next, s)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(ws.side, ws.ev_next, 0)) != cudaSuccess)
       return e;
@@ -374,17 +454,8 @@ cudaError_t enqueue_lu(int k, int m, int ncols, MatView A, int32_t *d_swaps,
       return e;
     if ((e = cudaEventRecord(ws.ev_panel, ws.side)) != cudaSuccess) return e;
     panel_pending = true;
-    // ... while this panel's exchanges, U12 and update finish elsewhere
-    if (split) {
-      if ((e = lu_laswp(k, A, 0, J, J2 + w2, ncols, sl, ws.status, s)) !=
-          cudaSuccess)
-        return e;
-    }
+    // ... while the rest of this panel's update runs here
     if (rest_c > w2) {
-      if (split &&
-          (e = lu_trsm(k, sub(A, J, J), sub(A, J, J2 + w2), w, rest_c - w2,
-                       ws.status, s)) != cudaSuccess)
-        return e;
       if ((e = lu_update(k, rest_r, rest_c - w2, w, sub(A, J2, J),
                          sub(A, J, J2 + w2), sub(A, J2, J2 + w2), ws.status,
                          s)) != cudaSuccess)
