@@ -209,6 +209,9 @@ int32_t mpcore_debug_panel_trace(uint64_t *out_ns, int64_t cap);
  * (MPCORE_TRACE_SOLVE set): [forward, backward][blocks][4] = start, completed
  * source blocks added, critical source block done, diagonal done */
 int32_t mpcore_debug_solve_trace(uint64_t *out_ns, int64_t cap);
+/* diagnostics: timeline of the profiled launches since mpcore_prof_reset,
+ * (slot, start us, end us) per launch in enqueue order */
+int32_t mpcore_debug_timeline(double *out, int64_t cap, int64_t *count);
 /* FP64 issue-rate microbenchmark: DADD instructions per second */
 int32_t mpcore_fp64_peak(double *dadd_per_s, double *dfma_per_s);
 

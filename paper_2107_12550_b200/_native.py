@@ -72,6 +72,8 @@ _PROTOS = {
     "mpcore_fp64_peak": (_i32, [_dp, _dp]),
     "mpcore_debug_panel_trace": (_i32, [ctypes.POINTER(_u64), _i64]),
     "mpcore_debug_solve_trace": (_i32, [ctypes.POINTER(_u64), _i64]),
+    "mpcore_debug_timeline": (_i32, [ctypes.POINTER(ctypes.c_double), _i64,
+                                     ctypes.POINTER(_i64)]),
     # device-pointer building blocks (dist.py)
     "mpcore_object_device_ptr": (_i32, [_u64, ctypes.POINTER(_u64)]),
     "mpcore_dev_lu_block": (_i32, [_i32, _i32, _i32, _u64, _i64, _i64, _i32,

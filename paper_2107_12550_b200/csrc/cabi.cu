@@ -166,7 +166,7 @@ int ensure_device_locked() {
     return fail(MPCORE_INTERNAL, D.why);
   }
   if (const char *t = std::getenv("MPCORE_TRACE_PANEL")) {
-    size_t bytes = (size_t)D.sms * 32 * 8 * sizeof(unsigned long long);
+    size_t bytes = (size_t)D.sms * 33 * 8 * sizeof(unsigned long long);
     if (cudaMalloc(&D.ws.trace, bytes) == cudaSuccess) {
       cudaMemset(D.ws.trace, 0, bytes);
       D.ws.trace_J = std::atoi(t);
@@ -317,6 +317,8 @@ struct Prof {
   double ms[mpk::PROF_NSLOTS] = {0};
   int64_t launches[mpk::PROF_NSLOTS] = {0};
   int pending[mpk::PROF_NSLOTS];
+  cudaEvent_t base = nullptr;     // timeline origin (set by prof_reset)
+  std::vector<double> timeline;   // (slot, start us, end us) per launch
   Prof() { for (int &p : pending) p = -1; }
   void collect() {
     for (auto &r : recs) {
@@ -325,6 +327,14 @@ struct Prof {
           cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) {
         ms[r.slot] += t;
         launches[r.slot] += 1;
+        float t0 = 0, t1 = 0;
+        if (base && timeline.size() < 3 * 200000 &&
+            cudaEventElapsedTime(&t0, base, r.a) == cudaSuccess &&
+            cudaEventElapsedTime(&t1, base, r.b) == cudaSuccess) {
+          timeline.push_back(r.slot);
+          timeline.push_back(1e3 * t0);
+          timeline.push_back(1e3 * t1);
+        }
       }
       cudaEventDestroy(r.a);
       cudaEventDestroy(r.b);
@@ -972,6 +982,22 @@ int32_t mpcore_prof_reset(void) {
     P.ms[i] = 0;
     P.launches[i] = 0;
   }
+  P.timeline.clear();
+  if (!P.base) cudaEventCreate(&P.base);
+  cudaEventRecord(P.base, device().stream);
+  return MPCORE_OK;
+}
+
+int32_t mpcore_debug_timeline(double *out, int64_t cap, int64_t *count) {
+  DevLock L;
+  if (L.st) return L.st;
+  Prof &P = prof();
+  P.collect();
+  const int64_t n = (int64_t)P.timeline.size();
+  if (count) *count = n / 3;
+  if (out) {
+    for (int64_t i = 0; i < n && i < cap; ++i) out[i] = P.timeline[i];
+  }
   return MPCORE_OK;
 }
 
@@ -979,7 +1005,7 @@ int32_t mpcore_debug_panel_trace(uint64_t *out_ns, int64_t cap) {
   DevLock L;
   if (L.st) return L.st;
   Device &D = device();
-  int64_t count = (int64_t)D.sms * 32 * 8;
+  int64_t count = (int64_t)D.sms * 33 * 8;
   if (!D.ws.trace) return fail(MPCORE_INTERNAL, "MPCORE_TRACE_PANEL not set");
   if (!out_ns || cap < count) return MPCORE_BAD_DIMENSION;
   cudaError_t e = cudaMemcpy(out_ns, D.ws.trace, count * sizeof(uint64_t),

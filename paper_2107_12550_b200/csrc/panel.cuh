@@ -77,6 +77,11 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31;
   if (ws.status[0] >= 0) return;
+  if (ws.trace != nullptr && ws.trace_J == J && tid == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    ws.trace[((int64_t)g * 33 + 32) * 8 + 0] = t;
+  }
   const unsigned seq0 = ws.epoch[0] * 65536u + (unsigned)J + 1u;
   const int m = n - J;
   const int R = (m + G - 1) / G;
@@ -84,10 +89,13 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
   const int nr = max(0, min(rbeg + R, n) - rbeg);
   const int rw = 2 * w * K;
   extern __shared__ double sm[];
-  double *rows = sm;                  // [R][W][K]
-  double *prow = rows + R * W * K;    // [W][K]
+  // [R][W*K + 1]: the odd row stride keeps warp 0's column accesses (lane =
+  // row) free of shared-memory bank conflicts
+  constexpr int RS = W * K + 1;
+  double *rows = sm;
+  double *prow = rows + R * RS;       // [W][K]
   __shared__ PanelSmem S;
-  auto at = [&](int r, int col) -> double * { return rows + (r * W + col) * K; };
+  auto at = [&](int r, int col) -> double * { return rows + r * RS + col * K; };
 
   for (int e = tid; e < nr * w; e += PANEL_THREADS) {
     int r = e / w, col = e % w;
@@ -152,10 +160,10 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       unsigned long long t;
       if (slot == 0) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        ws.trace[((int64_t)g * 32 + jj) * 8 + 7] = t;
+        ws.trace[((int64_t)g * 33 + jj) * 8 + 7] = t;
       }
       t = clock64();
-      ws.trace[((int64_t)g * 32 + jj) * 8 + slot] = t;
+      ws.trace[((int64_t)g * 33 + jj) * 8 + slot] = t;
     }
   };
   auto poll = [&](const u64 *p, unsigned seq) -> unsigned {
@@ -167,6 +175,14 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
     return (unsigned)(v >> 32);
   };
 
+  auto stamp = [&](int slot) {
+    if (tracing) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      ws.trace[((int64_t)g * 33 + 32) * 8 + slot] = t;
+    }
+  };
+  stamp(1);
   // prologue: candidate and rows of column 0 (all columns current)
   if (tid < 32) w0_publish_candidate(0, seq0);
   __syncthreads();
@@ -353,6 +369,7 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       nb_arrive(B_REM, PANEL_THREADS);
     }
   }
+  stamp(2);
   if (S.singular) return;  // uniform across the grid: no write-back
   __syncthreads();
   for (int e = tid; e < nr * w; e += PANEL_THREADS) {
@@ -361,43 +378,47 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
     for (int c = 0; c < K; ++c)
       A.p[c * A.plane + (int64_t)(rbeg + r) * A.ld + J + col] = at(r, col)[c];
   }
-  // Epilogue: CTA 0 composes the panel's row exchanges for laswp_kernel
-  // (after the exchanges row cur[i] holds what row src[i] held before).
+  // Epilogue: CTA 0 composes the panel's row exchanges for the exchange
+  // kernel: after the exchanges, row cur[i] holds what row src[i] held
+  // before.  Each lane traces one candidate position back through the
+  // swaps (J+jj <-> piv[jj], jj descending) -- no serial pass over columns.
   if (g == 0 && tid < 32) {
-    int ec0 = -1, es0 = -1, ec1 = -1, es1 = -1;  // lane entries l and l+32
-    int cnt = 0;
-    for (int jj = 0; jj < w; ++jj) {
-      const int a = J + jj, b = S.piv[jj];
-      if (a == b) continue;
-      unsigned fa = __ballot_sync(0xffffffffu, ec0 == a);
-      unsigned fa1 = __ballot_sync(0xffffffffu, ec1 == a);
-      unsigned fb = __ballot_sync(0xffffffffu, ec0 == b);
-      unsigned fb1 = __ballot_sync(0xffffffffu, ec1 == b);
-      int ia = fa ? __ffs(fa) - 1 : (fa1 ? 32 + __ffs(fa1) - 1 : -1);
-      int ib = fb ? __ffs(fb) - 1 : (fb1 ? 32 + __ffs(fb1) - 1 : -1);
-      if (ia < 0) {
-        ia = cnt++;
-        if (lane == (ia & 31)) {
-          if (ia < 32) { ec0 = a; es0 = a; } else { ec1 = a; es1 = a; }
-        }
+    const int pv = lane < w ? S.piv[lane] : -1;
+    auto origin = [&](int p) {
+      int x = p;
+#pragma unroll 4
+      for (int jj = w - 1; jj >= 0; --jj) {
+        const int b = __shfl_sync(0xffffffffu, pv, jj), a = J + jj;
+        x = x == a ? b : (x == b ? a : x);
       }
-      if (ib < 0) {
-        ib = cnt++;
-        if (lane == (ib & 31)) {
-          if (ib < 32) { ec0 = b; es0 = b; } else { ec1 = b; es1 = b; }
-        }
-      }
-      int sa = __shfl_sync(0xffffffffu, ia < 32 ? es0 : es1, ia & 31);
-      int sb = __shfl_sync(0xffffffffu, ib < 32 ? es0 : es1, ib & 31);
-      if (lane == (ia & 31)) { if (ia < 32) es0 = sb; else es1 = sb; }
-      if (lane == (ib & 31)) { if (ib < 32) es0 = sa; else es1 = sa; }
+      return x;
+    };
+    // positions: the panel rows J+lane, and each distinct pivot row below
+    const int pa = lane < w ? J + lane : -1;
+    int pb = -1;
+    if (lane < w && pv >= J + w) {
+      bool first = true;
+      for (int q = 0; q < lane; ++q)
+        if (S.piv[q] == pv) first = false;
+      if (first) pb = pv;
     }
+    const int sa = origin(pa), sb = origin(pb);
+    const bool ka = pa >= 0 && sa != pa, kb = pb >= 0 && sb != pb;
+    const unsigned ma = __ballot_sync(0xffffffffu, ka);
+    const unsigned mb = __ballot_sync(0xffffffffu, kb);
+    const unsigned lt = (1u << lane) - 1u;
     int32_t *sl = ws.swap_list + slot * LU_SWAP_LIST;
-    if (lane < cnt) { sl[lane] = ec0; sl[64 + lane] = es0; }
-    if (lane + 32 < cnt) {
-      sl[lane + 32] = ec1;
-      sl[64 + lane + 32] = es1;
+    if (ka) {
+      const int i = __popc(ma & lt);
+      sl[i] = pa;
+      sl[2 * LU_MAX_W + i] = sa;
     }
-    if (lane == 0) sl[128] = cnt;
+    if (kb) {
+      const int i = __popc(ma) + __popc(mb & lt);
+      sl[i] = pb;
+      sl[2 * LU_MAX_W + i] = sb;
+    }
+    if (lane == 0) sl[4 * LU_MAX_W] = __popc(ma) + __popc(mb);
   }
+  stamp(3);
 }

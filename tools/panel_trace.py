@@ -9,9 +9,10 @@ k = int(sys.argv[1]); n = int(sys.argv[2])
 A = DeviceMatrix(k, n, n); A.generate(0, n, 5)
 A.lu_factor()
 G = nat.sm_count()
-buf = np.zeros(G * 32 * 8, dtype=np.uint64)
+buf = np.zeros(G * 33 * 8, dtype=np.uint64)
 nat.check(nat.lib().mpcore_debug_panel_trace(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), buf.size), "trace")
-t = buf.reshape(G, 32, 8).astype(np.int64)
+t = buf.reshape(G, 33, 8).astype(np.int64)
+ks = t[:, 32, :4].copy()
 g_used = int((t[:, 0, 7] > 0).sum())
 t = t[:g_used]
 names = ["poll", "pivot+div", "B_ROW", "mult", "B_REM", "la+pub"]
@@ -24,3 +25,7 @@ per = np.median(np.diff(t[:, :31, 0], axis=1), axis=0); per = per[np.isfinite(pe
 print("period (cycles):", per[:10].astype(int), " median", int(np.median(per)))
 start_ns = t[:, :31, 7]
 print("period (ns, globaltimer):", np.median(np.diff(start_ns, axis=1), axis=0)[:10].astype(int))
+ks = ks[:g_used]
+e0 = ks[:, 0].min()
+print("kernel stamps (ns from first CTA entry; median/max over CTAs): entry %d/%d  prologue-done %d/%d  loop-done %d/%d  exit %d/%d" % tuple(
+    v for c in range(4) for v in (np.median(ks[:, c] - e0), (ks[:, c] - e0).max())))
