@@ -110,17 +110,7 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
   __syncthreads();
 
   // W0: local first max of column jj (rows >= J+jj) and its candidate words
-  auto w0_publish_candidate = [&](int jj, unsigned seq) {
-    const int j = J + jj;
-    double mag = -1.0;
-    int row = INT_MAX;
-    for (int r = lane; r < nr; r += 32) {
-      int gi = rbeg + r;
-      if (gi >= j) {
-        double v = fabs(at(r, jj)[0]);
-        if (better(v, gi, mag, row)) { mag = v; row = gi; }
-      }
-    }
+  auto w0_publish_max = [&](int jj, unsigned seq, double mag, int row) {
     double bm;
     int br;
     warp_argmax(mag, row, bm, br);
@@ -133,6 +123,19 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       const double v = br != INT_MAX ? at(br - rbeg, jj)[(lane - 1) >> 1] : 0.0;
       st_volatile(wd + lane, ll_word((lane & 1) ? lo32(v) : hi32(v), seq));
     }
+  };
+  auto w0_publish_candidate = [&](int jj, unsigned seq) {
+    const int j = J + jj;
+    double mag = -1.0;
+    int row = INT_MAX;
+    for (int r = lane; r < nr; r += 32) {
+      int gi = rbeg + r;
+      if (gi >= j) {
+        double v = fabs(at(r, jj)[0]);
+        if (better(v, gi, mag, row)) { mag = v; row = gi; }
+      }
+    }
+    w0_publish_max(jj, seq, mag, row);
   };
   // H: publish the candidate row of column jj (+ row J+jj if owned)
   auto h_publish_rows = [&](int jj, unsigned seq, int row) {
@@ -282,38 +285,44 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       trace(jj, 2);
       nb_sync(B_ROW, PANEL_THREADS);  // pivot row staged, swap applied
       trace(jj, 3);
-      // multipliers m_i = mul(A_ij, recip), rows i > j
+      // (H finished column jj-1 before it staged this pivot row, so this
+      // wait is only the barrier's bookkeeping)
+      if (jj >= 1) nb_sync(B_REM, PANEL_THREADS);
+      // one pass over the rows i > j: multiplier m_i = mul(A_ij, recip),
+      // look-ahead update of column jj+1 and its local first max
+      const bool ahead = jj + 1 < w;
+      double mag = -1.0;
+      int mrow = INT_MAX;
       for (int rr = lane; rr < nr; rr += 32) {
-        if (rbeg + rr > j) {
-          double a[K], o[K];
+        const int gi = rbeg + rr;
+        if (gi > j) {
+          double a[K], m[K];
 #pragma unroll
           for (int c = 0; c < K; ++c) a[c] = at(rr, jj)[c];
-          mc::mul<K>(a, rc, o);
+          mc::mul<K>(a, rc, m);
 #pragma unroll
-          for (int c = 0; c < K; ++c) at(rr, jj)[c] = o[c];
-        }
-      }
-      trace(jj, 4);
-      if (jj >= 1) nb_sync(B_REM, PANEL_THREADS);  // H done with column jj-1
-      trace(jj, 5);
-      if (jj + 1 < w) {
-        // look-ahead: column jj+1, then publish its candidate
-        for (int rr = lane; rr < nr; rr += 32) {
-          if (rbeg + rr > j) {
+          for (int c = 0; c < K; ++c) at(rr, jj)[c] = m[c];
+          if (ahead) {
             double negm[K], u[K], acc[K];
 #pragma unroll
             for (int c = 0; c < K; ++c) {
-              negm[c] = -at(rr, jj)[c];
+              negm[c] = -m[c];
               u[c] = prow[(jj + 1) * K + c];
               acc[c] = at(rr, jj + 1)[c];
             }
             mc::madd<K>(acc, negm, u);
 #pragma unroll
             for (int c = 0; c < K; ++c) at(rr, jj + 1)[c] = acc[c];
+            const double v = fabs(acc[0]);
+            if (better(v, gi, mag, mrow)) { mag = v; mrow = gi; }
           }
         }
+      }
+      trace(jj, 4);
+      trace(jj, 5);
+      if (ahead) {
         __syncwarp();
-        w0_publish_candidate(jj + 1, seq + 1);
+        w0_publish_max(jj + 1, seq + 1, mag, mrow);
         trace(jj, 6);
       }
       __syncwarp();
