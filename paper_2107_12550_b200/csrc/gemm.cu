@@ -109,7 +109,9 @@ gemm_kernel(int M, int N, int KK, MatView A, MatView B, MatView C,
     const double *As = smem + (kt & 1) * Cfg::STAGE;
     const double *Bs = As + K * Cfg::A_ELEMS;
     const int kmax = min(BK, KK - kt * BK);
-#pragma unroll 1
+    // small micro-tiles expose the accumulator chain: unroll so the products
+    // of the next steps overlap it
+#pragma unroll(TM * TN <= 2 ? 4 : 1)
     for (int kk = 0; kk < kmax; ++kk) {
       double a[TM][K], b[TN][K];
 #pragma unroll

@@ -218,22 +218,21 @@ swap_trsm_kernel(MatView A, int J, int w, int c0, int c1, int c2, int c3,
     src[tid] = swap_list[2 * LU_MAX_W + tid];
   }
   if (right) {
-    for (int e = tid; e < w * w; e += 128) {
-      const int r = e / w, q = e % w;
-      if (q < r) {
+    // L11 (strictly lower part, negated): 8 independent loads per thread
+#pragma unroll
+    for (int it = 0; it < (LU_MAX_W * LU_MAX_W) / 128; ++it) {
+      const int e = tid + 128 * it, r = e / LU_MAX_W, q = e % LU_MAX_W;
+      if (q < r && r < w) {
 #pragma unroll
         for (int k = 0; k < K; ++k)
           Ls[k][r][q] = -A.p[k * A.plane + (int64_t)(J + r) * A.ld + J + q];
       }
     }
+    if (tid < LU_MAX_W) rsrc[tid] = J + tid;
   }
   __syncthreads();
-  if (right && tid < w) {
-    int rs = J + tid;
-    for (int i = 0; i < cnt; ++i)
-      if (cur[i] == J + tid) rs = src[i];
-    rsrc[tid] = rs;
-  }
+  // the post-exchange source of each panel row (cur entries are distinct)
+  if (right && tid < cnt && cur[tid] < J + w) rsrc[cur[tid] - J] = src[tid];
   __syncthreads();
   if (col >= cend) return;
   const int64_t ld = A.ld;
