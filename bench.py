@@ -320,7 +320,10 @@ def run_ours(args):
                            "this GPU; nominal 148*64*1.965e9 = 18.6e12",
             "per_launch_avg_ms": upd_ms * args.steps / max(1, upd_launches),
             "update_share_of_step": upd_ms / ms if ms else None,
-            "traffic": None,
+            "traffic": traffic_bytes(k, n),
+            "traffic_note": "DRAM bytes of one captured update launch "
+                            "(profiles/r01_traffic.json; its algorithmic "
+                            "bytes are listed there)",
             "whole_step_frac": overall_rate / peak if peak else None,
         },
         "kernels_ms_per_step": {s: v[0] / args.steps for s, v in prof.items()
@@ -333,6 +336,17 @@ def run_ours(args):
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line))
+
+
+def traffic_bytes(k, n):
+    """dram__bytes_read + dram__bytes_write of the captured trailing-update
+    launch (ncu --set full), when the capture matches this workload."""
+    try:
+        d = json.load(open(os.path.join(os.path.dirname(os.path.abspath(
+            __file__)), "profiles", "r01_traffic.json")))
+    except (OSError, ValueError):
+        return None
+    return d["dram_bytes"] if (d.get("k"), d.get("n")) == (k, n) else None
 
 
 def run_dist(args):
