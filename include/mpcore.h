@@ -87,6 +87,26 @@ int32_t mpcore_report_solution_count(uint64_t h, int32_t *out);
 int32_t mpcore_report_solution_entry(uint64_t h, int32_t idx,
                                      int32_t digits, char *out, int32_t cap);
 
+/* ---- extension: BASELINE config 3 (TD-mpmath IR, n = 1024, κ = 1e30) ---
+ * Builds A = U diag(σ) W (σ geometric 1 .. 10^-kappa_exp10, U, W seeded
+ * butterfly-orthogonal at 576-bit fixed point) and b = A ones at long_bits
+ * on the host (threads <= 0: all), then runs the mpcore_refine loop on it
+ * (short side on the GPU).  Returns a report handle as mpcore_refine does. */
+int32_t mpcore_refine_config3(int32_t n, uint64_t seed, double kappa_exp10,
+                              int32_t short_k, int32_t long_bits,
+                              const char *rtol, const char *atol,
+                              int32_t max_iter, int32_t threads,
+                              uint64_t *report_out);
+/* the same system written as .mpmat files (BigFloat hex, matfile.py
+ * layout) for mpcore_refine or the reference's own driver; host only */
+int32_t mpcore_write_config3(int32_t n, uint64_t seed, double kappa_exp10,
+                             int32_t long_bits, int32_t threads,
+                             const char *a_path, const char *b_path);
+/* seconds: [generate, convert, factor, refinement loop, residuals, solves]
+ * (generate only for mpcore_refine_config3; mpcore_refine reports 5) */
+int32_t mpcore_report_timings(uint64_t h, double *out, int32_t cap,
+                              int32_t *count);
+
 /* ---- extensions: object introspection and bulk planar transfer --------- */
 
 /* kind: 1 matrix, 2 vector, 3 pivot record, 4 report */

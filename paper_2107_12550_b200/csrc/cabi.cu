@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -22,6 +23,7 @@
 #include "bignum.h"
 #include "internal.h"
 #include "refine_host.h"
+#include "testsys.h"
 
 namespace {
 
@@ -646,9 +648,65 @@ int32_t mpcore_refine(const char *a_path, const char *b_path, int32_t short_k,
   return MPCORE_OK;
 }
 
+int32_t mpcore_refine_config3(int32_t n, uint64_t seed, double kappa_exp10,
+                              int32_t short_k, int32_t long_bits,
+                              const char *rtol, const char *atol,
+                              int32_t max_iter, int32_t threads,
+                              uint64_t *report_out) {
+  if (report_out == nullptr) return MPCORE_BAD_DIMENSION;
+  *report_out = 0;
+  if (!rtol || !atol) return MPCORE_BAD_PARSE;
+  if (n < 1 || n > 65536) return MPCORE_BAD_DIMENSION;
+  auto rep = std::make_unique<mpr::Report>();
+  std::string err;
+  std::vector<bn::BF> A, b;
+  const auto t0 = std::chrono::steady_clock::now();
+  int st = mpr::config3_system(n, seed, long_bits, kappa_exp10, threads, A, b,
+                               err);
+  if (st) return fail(st, err);
+  const double t_gen = std::chrono::duration<double>(
+                           std::chrono::steady_clock::now() - t0)
+                           .count();
+  GpuShortSolver gpu;
+  st = mpr::refine_core(A, b, n, short_k, long_bits, rtol, atol, max_iter,
+                        threads, gpu, *rep, err);
+  if (st) return fail(st, err);
+  rep->timings.insert(rep->timings.begin(), t_gen);
+  auto o = std::make_shared<Object>();
+  o->kind = K_REPORT;
+  o->report = std::move(rep);
+  *report_out = table().put(o);
+  return MPCORE_OK;
+}
+
+int32_t mpcore_write_config3(int32_t n, uint64_t seed, double kappa_exp10,
+                             int32_t long_bits, int32_t threads,
+                             const char *a_path, const char *b_path) {
+  if (!a_path || !b_path) return MPCORE_BAD_PARSE;
+  if (n < 1 || n > 65536 || long_bits < 2) return MPCORE_BAD_DIMENSION;
+  std::string err;
+  std::vector<bn::BF> A, b;
+  int st = mpr::config3_system(n, seed, long_bits, kappa_exp10, threads, A, b,
+                               err);
+  if (!st) st = mpr::write_mpmat(a_path, A, n, n, long_bits, err);
+  if (!st) st = mpr::write_mpmat(b_path, b, n, 1, long_bits, err);
+  if (st) return fail(st, err);
+  return MPCORE_OK;
+}
+
 static mpr::Report *report_of(uint64_t h) {
   ObjPtr o = table().get(h, K_REPORT);
   return o ? o->report.get() : nullptr;
+}
+
+int32_t mpcore_report_timings(uint64_t h, double *out, int32_t cap,
+                              int32_t *count) {
+  mpr::Report *r = report_of(h);
+  if (!r) return MPCORE_BAD_HANDLE;
+  if (count) *count = (int32_t)r->timings.size();
+  for (int32_t i = 0; out && i < cap && i < (int32_t)r->timings.size(); ++i)
+    out[i] = r->timings[i];
+  return MPCORE_OK;
 }
 
 int32_t mpcore_report_iterations(uint64_t h, int32_t *out) {

@@ -44,7 +44,6 @@ namespace mpk {
 namespace {
 
 constexpr int PANEL_THREADS = 256;
-constexpr int NWARPS = PANEL_THREADS / 32;
 #ifndef POLL_NS
 #define POLL_NS 32
 #endif
@@ -71,33 +70,6 @@ __device__ __forceinline__ u64 ll_word(unsigned payload, unsigned seq) {
 // (np.argmax returns the first maximum, linalg.py:429).
 __device__ __forceinline__ bool better(double m1, int r1, double m2, int r2) {
   return m1 > m2 || (m1 == m2 && r1 < r2);
-}
-
-__device__ __forceinline__ void block_argmax(double &mag, int &row,
-                                             double *s_mag, int *s_row) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    double om = __shfl_down_sync(0xffffffffu, mag, off);
-    int orow = __shfl_down_sync(0xffffffffu, row, off);
-    if (better(om, orow, mag, row)) { mag = om; row = orow; }
-  }
-  if (lane == 0) { s_mag[wid] = mag; s_row[wid] = row; }
-  __syncthreads();
-  if (wid == 0) {
-    mag = lane < NWARPS ? s_mag[lane] : -1.0;
-    row = lane < NWARPS ? s_row[lane] : INT_MAX;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      double om = __shfl_down_sync(0xffffffffu, mag, off);
-      int orow = __shfl_down_sync(0xffffffffu, row, off);
-      if (better(om, orow, mag, row)) { mag = om; row = orow; }
-    }
-    if (lane == 0) { s_mag[NWARPS] = mag; s_row[NWARPS] = row; }
-  }
-  __syncthreads();
-  mag = s_mag[NWARPS];
-  row = s_row[NWARPS];
 }
 
 #include "panel.cuh"

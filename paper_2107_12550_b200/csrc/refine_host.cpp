@@ -8,10 +8,13 @@
 // ShortSolver (cabi.cu).
 #include "refine_host.h"
 
+#include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <fstream>
 #include <sstream>
+#include <thread>
 
 namespace mpr {
 
@@ -215,17 +218,84 @@ static int load_mpmat(const char *path, Loaded &L, std::string &err) {
   return 0;
 }
 
-// -------------------------------------------------------- the IR driver ----
-static int to_planes(const std::vector<BF> &v, int k, std::vector<double> &out,
-                     size_t count, std::string &err) {
-  out.assign((size_t)k * count, 0.0);
-  double c[4];
-  for (size_t e = 0; e < count; ++e) {
-    if (bn::to_multicomp(v[e], k, c)) {
-      err = "value does not fit in binary64";
-      return 5;
+// bf_format_hex (bigfloat.py:524-537): (+-)0x1.<nibbles>p(+-)E, exact
+std::string format_hex(const BF &a) {
+  if (a.sign == 0) return "0x0.0p+0";
+  const int64_t nbits = a.man.bits() - 1;
+  const int64_t e = a.exp + nbits;
+  std::string out = a.sign < 0 ? "-" : "";
+  char eb[32];
+  std::snprintf(eb, sizeof eb, "p%+lld", (long long)e);
+  if (nbits == 0) return out + "0x1" + eb;
+  const int64_t pad = (4 - nbits % 4) % 4;
+  // frac = (man - 2^nbits) << pad, printed as (nbits + pad) / 4 nibbles
+  const UBig frac = a.man.shl(pad);
+  const int64_t width = (nbits + pad) / 4;
+  std::string hex((size_t)width, '0');
+  static const char *dig = "0123456789abcdef";
+  for (int64_t i = 0; i < width; ++i) {
+    int v = 0;
+    for (int b = 0; b < 4; ++b) v |= (int)frac.bit(4 * i + b) << b;
+    hex[(size_t)(width - 1 - i)] = dig[v];
+  }
+  return out + "0x1." + hex + eb;
+}
+
+int write_mpmat(const char *path, const std::vector<BF> &vals, int rows,
+                int cols, int64_t bits, std::string &err) {
+  std::ofstream fh(path);
+  if (!fh) {
+    err = std::string(path) + ": cannot open for writing";
+    return 4;
+  }
+  fh << "mpmat " << rows << " " << cols << " bf " << bits << "\n";
+  for (int i = 0; i < rows; ++i) {
+    for (int j = 0; j < cols; ++j) {
+      if (j) fh << " ";
+      fh << format_hex(vals[(size_t)i * cols + j]);
     }
-    for (int q = 0; q < k; ++q) out[q * count + e] = c[q];
+    fh << "\n";
+  }
+  if (!fh) {
+    err = std::string(path) + ": write failed";
+    return 4;
+  }
+  return 0;
+}
+
+// -------------------------------------------------------- the IR driver ----
+// rows [0, n) split over host threads; every row keeps its own chain, so the
+// result does not depend on the thread count
+template <class F>
+static void par_rows(size_t n, int threads, F f) {
+  threads = (int)std::max<size_t>(1, std::min<size_t>((size_t)threads, n));
+  if (threads == 1) {
+    f((size_t)0, n);
+    return;
+  }
+  std::vector<std::thread> ts;
+  for (int t = 0; t < threads; ++t)
+    ts.emplace_back(f, n * t / threads, n * (t + 1) / threads);
+  for (auto &t : ts) t.join();
+}
+
+static int to_planes(const std::vector<BF> &v, int k, std::vector<double> &out,
+                     size_t count, std::string &err, int threads = 1) {
+  out.assign((size_t)k * count, 0.0);
+  std::vector<char> bad(threads > 0 ? threads : 1, 0);
+  par_rows(count, threads, [&](size_t a, size_t b) {
+    double c[4];
+    for (size_t e = a; e < b; ++e) {
+      if (bn::to_multicomp(v[e], k, c)) {
+        bad[0] = 1;  // any thread: the value is reported below
+        return;
+      }
+      for (int q = 0; q < k; ++q) out[q * count + e] = c[q];
+    }
+  });
+  if (bad[0]) {
+    err = "value does not fit in binary64";
+    return 5;
   }
   return 0;
 }
@@ -236,26 +306,22 @@ static BF norm2(const std::vector<BF> &v, int64_t p) {
   return lf_sqrt(acc, p);
 }
 
-int refine_files(const char *a_path, const char *b_path, int short_k,
-                 int long_bits, const char *rtol_s, const char *atol_s,
-                 int max_iter, ShortSolver &S, Report &out, std::string &err) {
-  Loaded A, B;
-  int st = load_mpmat(a_path, A, err);
-  if (st) return st;
-  st = load_mpmat(b_path, B, err);
-  if (st) return st;
-  if (B.cols != 1) {
-    err = std::string(b_path) + ": vector file must have 1 column";
-    return 4;
-  }
+using Clock = std::chrono::steady_clock;
+static double secs(Clock::time_point a, Clock::time_point b) {
+  return std::chrono::duration<double>(b - a).count();
+}
+
+int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
+                int short_k, int long_bits, const char *rtol_s,
+                const char *atol_s, int max_iter, int threads, ShortSolver &S,
+                Report &out, std::string &err) {
+  if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  int st;
   // RefineConfig validation (refine.py:70-77): DomainError -> 6
   if (short_k < 2 || short_k > 4) { err = "short_k must be 2, 3, or 4"; return 6; }
   if (long_bits <= 53 * short_k) { err = "long_bits must exceed 53 * short_k"; return 6; }
   if (max_iter < 1) { err = "max_iter must be >= 1"; return 6; }
-  if (!A.bf || !B.bf) { err = "refinement expects BigFloat matrix and vector"; return 6; }
-  if (A.rows != A.cols) { err = "matrix must be square"; return 2; }
-  if (B.rows != A.rows) { err = "rhs length does not match n"; return 2; }
-  const int n = A.rows, k = short_k;
+  const int k = short_k;
   const int64_t p = long_bits;
   BF rtol, atol;
   if (bn::parse_decimal(rtol_s, p, rtol) || bn::parse_decimal(atol_s, p, atol)) {
@@ -264,16 +330,28 @@ int refine_files(const char *a_path, const char *b_path, int short_k,
   }
   if (rtol.sign < 0 || atol.sign < 0) { err = "tolerances must be nonnegative"; return 6; }
   if (rtol.sign == 0 && atol.sign == 0) { err = "rtol and atol cannot both be zero"; return 6; }
+  const auto t0 = Clock::now();
   // re-round into the working context (convert_* BfDomain -> BfDomain)
-  for (auto &v : A.vals) v = lf_round(v, p);
-  for (auto &v : B.vals) v = lf_round(v, p);
+  par_rows(Avals.size(), threads, [&](size_t a, size_t b) {
+    for (size_t e = a; e < b; ++e) Avals[e] = lf_round(Avals[e], p);
+  });
+  for (auto &v : Bvals) v = lf_round(v, p);
   // short copies; transfer precision max(long, 53k+64)+8 (linalg.py:743)
   const int64_t p_in = std::max<int64_t>(p, 53 * k + 64) + 8;
   std::vector<double> a_pl, b_pl, x_pl;
-  if ((st = to_planes(A.vals, k, a_pl, (size_t)n * n, err))) return st;
-  if ((st = to_planes(B.vals, k, b_pl, (size_t)n, err))) return st;
+  if ((st = to_planes(Avals, k, a_pl, (size_t)n * n, err, threads))) return st;
+  if ((st = to_planes(Bvals, k, b_pl, (size_t)n, err))) return st;
+  const auto t1 = Clock::now();
   if ((st = S.factor(k, n, a_pl, err))) return st;
-  if ((st = S.solve(b_pl, x_pl, err))) return st;
+  const auto t2 = Clock::now();
+  double t_solve = 0, t_res = 0;
+  auto timed_solve = [&](const std::vector<double> &rhs) {
+    const auto a = Clock::now();
+    const int r = S.solve(rhs, x_pl, err);
+    t_solve += secs(a, Clock::now());
+    return r;
+  };
+  if ((st = timed_solve(b_pl))) return st;
   auto lift = [&](const std::vector<double> &pl, std::vector<BF> &x) {
     x.resize(n);
     double c[4];
@@ -285,10 +363,16 @@ int refine_files(const char *a_path, const char *b_path, int short_k,
   std::vector<BF> x;
   lift(x_pl, x);
   // ||A||_F, row-major accumulation (linalg.py:692-700)
+  // (the squares are independent: formed on all threads, then summed in
+  // the reference's order)
   BF a_fro;
   {
+    std::vector<BF> sq(Avals.size());
+    par_rows(Avals.size(), threads, [&](size_t a, size_t b) {
+      for (size_t e = a; e < b; ++e) sq[e] = lf_mul(Avals[e], Avals[e], p);
+    });
     BF acc;
-    for (const BF &s : A.vals) acc = lf_add(acc, lf_mul(s, s, p), p);
+    for (const BF &s : sq) acc = lf_add(acc, s, p);
     a_fro = lf_sqrt(acc, p);
   }
   const BF one = from_int(1, p);
@@ -298,13 +382,17 @@ int refine_files(const char *a_path, const char *b_path, int short_k,
   int corrections = 0;
   out.residuals.clear();
   for (int it = 0; it < max_iter; ++it) {
-    // res = b - A x  (scalar mat_vec order, linalg.py:566-574)
-    for (int i = 0; i < n; ++i) {
-      BF acc;
-      const BF *row = &A.vals[(size_t)i * n];
-      for (int j = 0; j < n; ++j) acc = lf_add(acc, lf_mul(row[j], x[j], p), p);
-      res[i] = lf_sub(B.vals[i], acc, p);
-    }
+    // res = b - A x  (scalar mat_vec order per row, linalg.py:566-574)
+    const auto ta = Clock::now();
+    par_rows((size_t)n, threads, [&](size_t r0, size_t r1) {
+      for (size_t i = r0; i < r1; ++i) {
+        BF acc;
+        const BF *row = &Avals[i * n];
+        for (int j = 0; j < n; ++j) acc = lf_add(acc, lf_mul(row[j], x[j], p), p);
+        res[i] = lf_sub(Bvals[i], acc, p);
+      }
+    });
+    t_res += secs(ta, Clock::now());
     BF res_norm = norm2(res, p);
     out.residuals.push_back(res_norm);
     if (res_norm.sign == 0) { reason = "converged"; break; }
@@ -326,16 +414,41 @@ int refine_files(const char *a_path, const char *b_path, int short_k,
     for (int i = 0; i < n; ++i) work[i] = lf_mul(res[i], coef, p);
     std::vector<double> w_pl;
     if ((st = to_planes(work, k, w_pl, (size_t)n, err))) return st;
-    if ((st = S.solve(w_pl, x_pl, err))) return st;
+    if ((st = timed_solve(w_pl))) return st;
     lift(x_pl, z);
     for (int i = 0; i < n; ++i) x[i] = lf_add(x[i], lf_mul(z[i], res_norm, p), p);
     ++corrections;
   }
+  const auto t3 = Clock::now();
   out.iterations = corrections;
   out.stop_reason = reason;
   out.solution = x;
   out.prec = p;
+  // convert, factor, refinement loop (incl. first solve), residuals, solves
+  out.timings = {secs(t0, t1), secs(t1, t2), secs(t2, t3), t_res, t_solve};
   return 0;
+}
+
+int refine_files(const char *a_path, const char *b_path, int short_k,
+                 int long_bits, const char *rtol_s, const char *atol_s,
+                 int max_iter, ShortSolver &S, Report &out, std::string &err) {
+  Loaded A, B;
+  int st = load_mpmat(a_path, A, err);
+  if (st) return st;
+  st = load_mpmat(b_path, B, err);
+  if (st) return st;
+  if (B.cols != 1) {
+    err = std::string(b_path) + ": vector file must have 1 column";
+    return 4;
+  }
+  if (short_k < 2 || short_k > 4) { err = "short_k must be 2, 3, or 4"; return 6; }
+  if (long_bits <= 53 * short_k) { err = "long_bits must exceed 53 * short_k"; return 6; }
+  if (max_iter < 1) { err = "max_iter must be >= 1"; return 6; }
+  if (!A.bf || !B.bf) { err = "refinement expects BigFloat matrix and vector"; return 6; }
+  if (A.rows != A.cols) { err = "matrix must be square"; return 2; }
+  if (B.rows != A.rows) { err = "rhs length does not match n"; return 2; }
+  return refine_core(A.vals, B.vals, A.rows, short_k, long_bits, rtol_s,
+                     atol_s, max_iter, 0, S, out, err);
 }
 
 }  // namespace mpr

@@ -18,6 +18,9 @@ struct Report {
   std::vector<bn::BF> residuals;   // residual 2-norm per iteration
   std::vector<bn::BF> solution;    // final x at long precision
   int64_t prec = 0;                // precision of residuals / solution
+  // seconds: generate (config 3 only), convert, factor, refinement loop,
+  // residuals (inside the loop), short solves (inside the loop)
+  std::vector<double> timings;
 };
 
 // The short side: factor once, solve many (implemented on the GPU by
@@ -37,6 +40,19 @@ int refine_files(const char *a_path, const char *b_path, int short_k,
                  int long_bits, const char *rtol, const char *atol,
                  int max_iter, ShortSolver &short_side, Report &out,
                  std::string &err);
+
+// the refinement loop on long-precision values already in memory (A
+// row-major n x n, B length n); threads <= 0: all host threads
+int refine_core(std::vector<bn::BF> &A, std::vector<bn::BF> &B, int n,
+                int short_k, int long_bits, const char *rtol, const char *atol,
+                int max_iter, int threads, ShortSolver &short_side, Report &out,
+                std::string &err);
+
+// bf_format_hex (bigfloat.py:524-537) and a .mpmat writer (matfile.py
+// layout: header "mpmat rows cols bf bits", one row per line)
+std::string format_hex(const bn::BF &v);
+int write_mpmat(const char *path, const std::vector<bn::BF> &vals, int rows,
+                int cols, int64_t bits, std::string &err);
 
 // bf_format_decimal (bigfloat.py:483-509); digits <= 0: the default for prec
 std::string format_decimal(const bn::BF &v, int digits, int64_t prec);

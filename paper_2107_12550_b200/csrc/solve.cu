@@ -34,7 +34,6 @@ namespace mpk {
 namespace {
 
 constexpr int SB = 32;         // rows per block (owner lanes)
-constexpr int CH = 8;          // critical-block rows fetched per round trip
 constexpr int NPW = 3;         // producer warps
 constexpr int ST = 32 * (1 + NPW);
 constexpr int PS = SB + 1;     // padded row stride of the shared tiles
