@@ -52,12 +52,14 @@ def work_counts(n, k):
 
 
 def update_madds(n, nb):
-    """madds executed by the trailing-update kernel over one LU."""
+    """madds of the wide trailing-update launches over one LU (profile slot
+    "update"; the look-ahead's next-panel columns are slot "update_next")."""
     t = 0
     for J in range(0, n, nb):
         w = min(nb, n - J)
         rest = n - J - w
-        t += rest * rest * w
+        w2 = min(nb, rest)
+        t += rest * (rest - w2) * w
     return t
 
 
@@ -313,7 +315,8 @@ def run_ours(args):
                         "get_planes(x), pinned host buffers"},
         "roofline": {
             "bound": "fp64",
-            "kernel": "trailing update (gemm_kernel NEG_A)",
+            "kernel": "trailing update, wide launches (gemm_kernel NEG_A; "
+                      "main stream)",
             "achieved": upd_rate / 1e12, "peak": peak / 1e12,
             "unit": "T FP64 instr/s", "frac": upd_rate / peak if peak else None,
             "peak_source": "measured DADD issue rate (mpcore_fp64_peak) on "

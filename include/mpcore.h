@@ -218,7 +218,8 @@ int32_t mpcore_last_error(char *out, int32_t cap);
 int32_t mpcore_sync(void);
 /* per-kernel-family CUDA-event timing on the library stream:
  * slots 0 panel, 1 laswp, 2 trsm, 3 trailing update, 4 solve, 5 gemm,
- * 6 mat_vec, 7 elementwise, 8 generator */
+ * 6 mat_vec, 7 elementwise, 8 generator, 9 the look-ahead's next-panel
+ * update (the rest of the trailing update is slot 3) */
 int32_t mpcore_prof_enable(int32_t on);
 int32_t mpcore_prof_reset(void);
 int32_t mpcore_prof_read(double *ms, int64_t *launches, int32_t cap);

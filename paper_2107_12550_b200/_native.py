@@ -264,7 +264,7 @@ class PinnedBuffer:
 
 
 PROF_SLOTS = ["panel", "laswp", "trsm", "update", "solve", "gemm", "matvec",
-              "elementwise", "gen"]
+              "elementwise", "gen", "update_next"]
 
 
 def prof_enable(on=True):

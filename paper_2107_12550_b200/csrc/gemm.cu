@@ -322,9 +322,10 @@ cudaError_t gemm(int k, bool neg_a, bool zero_init, int M, int N, int KK,
 }
 
 cudaError_t lu_update(int k, int M, int N, int w, MatView L21, MatView U12,
-                      MatView A22, const int32_t *status, cudaStream_t s) {
+                      MatView A22, const int32_t *status, cudaStream_t s,
+                      int prof_slot) {
   if (M <= 0 || N <= 0 || w <= 0) return cudaSuccess;
-  prof_begin(PROF_UPDATE, s);
+  prof_begin(prof_slot, s);
   cudaError_t e = cudaErrorInvalidValue;
   switch (k) {
     case 2: e = launch<2, true, false>(M, N, w, L21, U12, A22, status, s, update_mask(2)); break;
@@ -332,7 +333,7 @@ cudaError_t lu_update(int k, int M, int N, int w, MatView L21, MatView U12,
     case 4: e = launch<4, true, false>(M, N, w, L21, U12, A22, status, s, update_mask(4)); break;
     default: break;
   }
-  prof_end(PROF_UPDATE, s);
+  prof_end(prof_slot, s);
   return e;
 }
 

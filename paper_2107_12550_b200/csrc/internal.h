@@ -16,7 +16,8 @@ struct MatView {
 // Kernel timing accumulator (CUDA events on the library stream).
 enum ProfSlot {
   PROF_PANEL = 0, PROF_LASWP, PROF_TRSM, PROF_UPDATE, PROF_SOLVE,
-  PROF_GEMM, PROF_MATVEC, PROF_ELEMENTWISE, PROF_GEN, PROF_NSLOTS
+  PROF_GEMM, PROF_MATVEC, PROF_ELEMENTWISE, PROF_GEN, PROF_UPDATE_NEXT,
+  PROF_NSLOTS
 };
 void prof_begin(int slot, cudaStream_t s);
 void prof_end(int slot, cudaStream_t s);
@@ -108,6 +109,7 @@ cudaError_t lu_laswp(int k, MatView A, int c0, int c1, int c2, int c3,
 cudaError_t lu_trsm(int k, MatView L11, MatView U12, int w, int ncols,
                     const int32_t *status, cudaStream_t s);
 cudaError_t lu_update(int k, int M, int N, int w, MatView L21, MatView U12,
-                      MatView A22, const int32_t *status, cudaStream_t s);
+                      MatView A22, const int32_t *status, cudaStream_t s,
+                      int prof_slot = PROF_UPDATE);
 
 }  // namespace mpk

@@ -428,14 +428,16 @@ cudaError_t enqueue_lu(int k, int m, int ncols, MatView A, int32_t *d_swaps,
     cudaStream_t ns = next_on_main ? s : ws.side;
     if (next_on_main &&
         (e = lu_update(k, rest_r, w2, w, sub(A, J2, J), sub(A, J, J2),
-                       sub(A, J2, J2), ws.status, s)) != cudaSuccess)
+                       sub(A, J2, J2), ws.status, s, PROF_UPDATE_NEXT)) !=
+            cudaSuccess)
       return e;
     if ((e = cudaEventRecord(ws.ev_next, s)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(ws.side, ws.ev_next, 0)) != cudaSuccess)
       return e;
     if (!next_on_main &&
         (e = lu_update(k, rest_r, w2, w, sub(A, J2, J), sub(A, J, J2),
-                       sub(A, J2, J2), ws.status, ns)) != cudaSuccess)
+                       sub(A, J2, J2), ws.status, ns, PROF_UPDATE_NEXT)) !=
+            cudaSuccess)
       return e;
     if ((e = lu_panel(k, m, A, J2, w2, d_swaps, ws, slot ^ 1, ws.side)) !=
         cudaSuccess)

@@ -357,20 +357,30 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       nb_arrive(B_ROW, PANEL_THREADS);
       nb_sync(B_MUL, PANEL_THREADS);   // multipliers + next candidate known
       if (jj + 1 >= w) break;
+      // remaining rank-1 update, columns jj+2 .. w-1 of the rows i > j: a
+      // thread keeps one column's pivot-row value and walks a strided set of
+      // rows (independent madds, unrolled for ILP)
       const int ncol = w - jj - 2;
-      for (int e = ht; e < nr * ncol; e += H_THREADS) {
-        int rr = e / ncol, cc = jj + 2 + e % ncol;
-        if (rbeg + rr > j) {
-          double negm[K], u[K], acc[K];
+      if (ncol > 0) {
+        const int ng = H_THREADS / ncol;
+        const int cc = jj + 2 + ht % ncol, g0 = ht / ncol;
+        const int r_first = max(0, j + 1 - rbeg);
+        if (g0 < ng) {
+          double u[K];
 #pragma unroll
-          for (int c = 0; c < K; ++c) {
-            negm[c] = -at(rr, jj)[c];
-            u[c] = prow[cc * K + c];
-            acc[c] = at(rr, cc)[c];
+          for (int c = 0; c < K; ++c) u[c] = prow[cc * K + c];
+#pragma unroll 4
+          for (int rr = r_first + g0; rr < nr; rr += ng) {
+            double negm[K], acc[K];
+#pragma unroll
+            for (int c = 0; c < K; ++c) {
+              negm[c] = -at(rr, jj)[c];
+              acc[c] = at(rr, cc)[c];
+            }
+            mc::madd<K>(acc, negm, u);
+#pragma unroll
+            for (int c = 0; c < K; ++c) at(rr, cc)[c] = acc[c];
           }
-          mc::madd<K>(acc, negm, u);
-#pragma unroll
-          for (int c = 0; c < K; ++c) at(rr, cc)[c] = acc[c];
         }
       }
       nb_sync(B_H, H_THREADS);
