@@ -1,0 +1,37 @@
+"""Parity at the benchmark sizes: the exact bench workloads (BASELINE
+config 2, TD n = 2048 with the bench seed; DD n = 4096, whose panels span
+128 CTAs) factored and solved on the GPU must equal the oracle bit for bit
+-- pivots, factors and solution.  The oracle (C++ restatement, OpenMP over
+rows) needs ~10-20 s per case on the GPU box's host cores."""
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import gen
+from paper_2107_12550_b200 import _native as nat
+from paper_2107_12550_b200.linalg import DeviceMatrix, DeviceVector, device_solve
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("k,n,seed", [(3, 2048, 210712552), (2, 4096, 77)])
+def test_bench_workload_bitwise(k, n, seed):
+    # the bench's own inputs: device generator + device mat_vec
+    A0 = DeviceMatrix(k, n, n)
+    A0.generate(0, n, seed)
+    xt = DeviceVector(k, n)
+    xt.generate(2, n, seed)
+    b = DeviceVector(k, n)
+    nat.check(nat.lib().mpcore_mat_vec(A0.handle, xt.handle, b.handle), "mv")
+    A = A0.download()
+    bh = b.download()
+    assert A.tobytes() == gen.planes(k, (n, n), 0, n, seed).tobytes()
+    assert bh.tobytes() == oracle.matvec(A, xt.download()).tobytes()
+    piv = A0.lu_factor()
+    x = DeviceVector(k, n)
+    device_solve(A0, piv, b, x)
+    lu_ref, sw_ref = oracle.lu(A)
+    assert np.asarray(piv.swaps()).tobytes() == sw_ref.tobytes()
+    assert A0.download().tobytes() == lu_ref.tobytes()
+    assert x.download().tobytes() == oracle.solve(lu_ref, sw_ref, bh).tobytes()
