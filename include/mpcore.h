@@ -87,6 +87,23 @@ int32_t mpcore_report_solution_count(uint64_t h, int32_t *out);
 int32_t mpcore_report_solution_entry(uint64_t h, int32_t idx,
                                      int32_t digits, char *out, int32_t cap);
 
+/* ---- extension: one-call solve ----------------------------------------
+ * x = A^-1 b with A's factors left in A and the pivot record returned, as
+ * mpcore_lu_factor + mpcore_lu_solve do (bit for bit); b rides along as an
+ * extra column of the factorisation (its exchanges and updates are the
+ * forward substitution, element by element in the reference's order), so
+ * only the back substitution runs after the LU.  nb <= 0: default. */
+int32_t mpcore_solve_system(uint64_t a_h, uint64_t b_h, uint64_t x_h,
+                            int32_t nb, uint64_t *piv_out,
+                            int32_t *singular_step);
+/* the same on a caller-owned augmented device matrix [A | b] (k planes of
+ * n x ld, ld >= n+1, b in column n): factors in place, x (k x n planar)
+ * out, swaps_out (n entries, may be NULL) */
+int32_t mpcore_dev_solve_system(int32_t k, int32_t n, uint64_t aug,
+                                int64_t ld, int64_t plane, int32_t nb,
+                                uint64_t x, int32_t *swaps_out,
+                                int32_t *singular_step);
+
 /* ---- extension: BASELINE config 3 (TD-mpmath IR, n = 1024, κ = 1e30) ---
  * Builds A = U diag(σ) W (σ geometric 1 .. 10^-kappa_exp10, U, W seeded
  * butterfly-orthogonal at 576-bit fixed point) and b = A ones at long_bits

@@ -7,6 +7,7 @@
 // planes in device memory; all compute runs on the library's CUDA stream.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -111,6 +112,8 @@ struct Device {
   size_t tmp_bytes = 0;
   int32_t *dswaps = nullptr;  // LU swap output (stable for graph replay)
   int swaps_cap = 0;
+  double *aug = nullptr;      // [A | b] workspace of mpcore_solve_system
+  size_t aug_bytes = 0;
 };
 
 Device &device() {
@@ -491,6 +494,50 @@ int32_t mpcore_lu_factor_ex(uint64_t h, int32_t nb, uint64_t *piv_out,
   }
 }
 
+static mpk::MatView mv(uint64_t base, int64_t ld, int64_t plane);
+
+// Factor the augmented n x (n+1) matrix [A | b] at aug in place -- the
+// right-hand side follows every exchange and update, which is the forward
+// substitution of the reference's lu_solve, element by element in its order
+// -- then back-substitute into x (planar k x n).  -> status (3 singular)
+int solve_augmented_locked(int k, int n, double *aug, int64_t ld,
+                           int64_t plane, double *x, int nb,
+                           std::vector<int32_t> &swaps, int32_t *sing) {
+  Device &D = device();
+  cudaError_t e;
+  if (D.swaps_cap < n) {
+    if (D.dswaps) cudaFree(D.dswaps);
+    D.dswaps = nullptr;
+    D.swaps_cap = 0;
+    if ((e = cudaMalloc(&D.dswaps, (size_t)n * sizeof(int32_t))) != cudaSuccess)
+      return cuda_fail(e, "cudaMalloc(swaps)");
+    D.swaps_cap = n;
+  }
+  int32_t step = -1;
+  e = mpk::lu_factor(k, n, n + 1, mv((uint64_t)aug, ld, plane), D.dswaps,
+                     nb > 0 ? nb : default_nb(k, n), D.ws, &step, D.stream);
+  if (e != cudaSuccess) return cuda_fail(e, "lu_factor");
+  if (sing) *sing = step;
+  if (step >= 0)
+    return fail(MPCORE_SINGULAR,
+                "no nonzero pivot at elimination step " + std::to_string(step));
+  for (int c = 0; c < k && e == cudaSuccess; ++c)
+    e = cudaMemcpy2DAsync(x + (size_t)c * n, sizeof(double),
+                          aug + (size_t)c * plane + n, (size_t)ld * 8, 8, n,
+                          cudaMemcpyDeviceToDevice, D.stream);
+  if (e == cudaSuccess)
+    e = mpk::lu_solve_back(k, n, mv((uint64_t)aug, ld, plane), x, D.sw,
+                           D.stream);
+  if (e != cudaSuccess) return cuda_fail(e, "solve_back");
+  swaps.assign(n, 0);
+  e = cudaMemcpyAsync(swaps.data(), D.dswaps, n * sizeof(int32_t),
+                      cudaMemcpyDeviceToHost, D.stream);
+  int st = finish("solve_system");
+  if (st) return st;
+  if (e != cudaSuccess) return cuda_fail(e, "swaps download");
+  return MPCORE_OK;
+}
+
 int32_t mpcore_lu_factor(uint64_t h, uint64_t *piv_out) {
   return mpcore_lu_factor_ex(h, 0, piv_out, nullptr);
 }
@@ -628,6 +675,85 @@ class GpuShortSolver : public mpr::ShortSolver {
 }  // namespace
 
 extern "C" {
+
+int32_t mpcore_solve_system(uint64_t a_h, uint64_t b_h, uint64_t x_h,
+                            int32_t nb, uint64_t *piv_out,
+                            int32_t *singular_step) {
+  if (piv_out == nullptr) return MPCORE_BAD_DIMENSION;
+  *piv_out = 0;
+  if (singular_step) *singular_step = -1;
+  ObjPtr b = table().get(b_h, K_VECTOR);
+  if (!b) return MPCORE_BAD_HANDLE;
+  ObjPtr a, x;
+  int st = table().latch(a_h, K_MATRIX, a);
+  if (st) return st;
+  struct Unlatch {
+    ObjPtr &o;
+    ~Unlatch() { if (o) table().unlatch(o); }
+  } ua{a};
+  st = table().latch(x_h, K_VECTOR, x);
+  if (st) return st;
+  Unlatch ux{x};
+  const int n = a->rows, k = a->k;
+  if (a->rows != a->cols || b->rows != n || x->rows != n || b->k != k ||
+      x->k != k)
+    return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  Device &D = device();
+  const int64_t ld = n + 1, plane = (int64_t)n * ld;
+  const size_t bytes = (size_t)k * plane * sizeof(double);
+  cudaError_t e = cudaSuccess;
+  if (D.aug_bytes < bytes) {
+    if (D.aug) cudaFree(D.aug);
+    D.aug = nullptr;
+    D.aug_bytes = 0;
+    if ((e = cudaMalloc(&D.aug, bytes)) != cudaSuccess)
+      return cuda_fail(e, "cudaMalloc(augmented)");
+    D.aug_bytes = bytes;
+  }
+  for (int c = 0; c < k && e == cudaSuccess; ++c) {
+    e = cudaMemcpy2DAsync(D.aug + c * plane, ld * 8, a->d + (size_t)c * n * n,
+                          (size_t)n * 8, (size_t)n * 8, n,
+                          cudaMemcpyDeviceToDevice, D.stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(D.aug + c * plane + n, ld * 8, b->d + (size_t)c * n,
+                            8, 8, n, cudaMemcpyDeviceToDevice, D.stream);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "augment");
+  std::vector<int32_t> swaps;
+  st = solve_augmented_locked(k, n, D.aug, ld, plane, x->d, nb, swaps,
+                              singular_step);
+  if (st) return st;
+  // the factors back into A, as mpcore_lu_factor leaves them
+  for (int c = 0; c < k && e == cudaSuccess; ++c)
+    e = cudaMemcpy2DAsync(a->d + (size_t)c * n * n, (size_t)n * 8,
+                          D.aug + c * plane, ld * 8, (size_t)n * 8, n,
+                          cudaMemcpyDeviceToDevice, D.stream);
+  if (e != cudaSuccess) return cuda_fail(e, "factors copy");
+  st = finish("solve_system");
+  if (st) return st;
+  return make_pivot(swaps, piv_out);
+}
+
+int32_t mpcore_dev_solve_system(int32_t k, int32_t n, uint64_t aug,
+                                int64_t ld, int64_t plane, int32_t nb,
+                                uint64_t x, int32_t *swaps_out,
+                                int32_t *singular_step) {
+  if (k < 2 || k > 4 || n < 1 || !aug || !x || ld < n + 1 ||
+      plane < (int64_t)n * ld)
+    return MPCORE_BAD_DIMENSION;
+  if (singular_step) *singular_step = -1;
+  DevLock L;
+  if (L.st) return L.st;
+  std::vector<int32_t> swaps;
+  int st = solve_augmented_locked(k, n, reinterpret_cast<double *>(aug), ld,
+                                  plane, reinterpret_cast<double *>(x), nb,
+                                  swaps, singular_step);
+  if (st) return st;
+  if (swaps_out) std::copy(swaps.begin(), swaps.end(), swaps_out);
+  return MPCORE_OK;
+}
 
 int32_t mpcore_refine(const char *a_path, const char *b_path, int32_t short_k,
                       int32_t long_bits, const char *rtol, const char *atol,

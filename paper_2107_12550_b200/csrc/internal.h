@@ -96,6 +96,11 @@ cudaError_t lu_solve(int k, int n, MatView LU, const int32_t *d_perm,
                      const double *b, double *x, SolveWork &sw,
                      cudaStream_t s);
 
+// back substitution only: x (planar k x n) holds L^-1 P b on entry (e.g.
+// the right-hand-side column of an augmented LU) and x on exit
+cudaError_t lu_solve_back(int k, int n, MatView LU, double *x, SolveWork &sw,
+                          cudaStream_t s);
+
 // panel pieces (exposed for the distributed driver)
 cudaError_t lu_begin(LuWork &ws, cudaStream_t s);
 // factor panel [J, J+w); its composed row exchanges go to swap-list slot

@@ -376,9 +376,12 @@ cudaError_t lu_swap_trsm(int k, MatView A, int J, int w, int c0, int c1,
   return cudaGetLastError();
 }
 
-// LU of the m x ncols matrix A (ncols <= m): ncols == m is the square
-// factorisation; ncols < m factors a tall block (the distributed LU's
-// panel), pivoting over all m rows and exchanging rows inside the block.
+// LU of the m x ncols matrix A: ncols == m is the square factorisation;
+// ncols < m factors a tall block (the distributed LU's panel), pivoting over
+// all m rows and exchanging rows inside the block; ncols > m carries the
+// columns beyond m as right-hand sides: they get every row exchange and
+// every update (exactly the forward substitution of L y = P b, element by
+// element in the reference's order) but no pivots.
 //
 // Look-ahead (HPL style): after panel P's exchanges and TRSM, the trailing
 // update is split into the next panel's columns ("next") and the rest.  The
@@ -393,8 +396,9 @@ cudaError_t enqueue_lu(int k, int m, int ncols, MatView A, int32_t *d_swaps,
                      std::getenv("MPCORE_NO_LOOKAHEAD") == nullptr;
   if ((e = lu_begin(ws, s)) != cudaSuccess) return e;
   bool panel_pending = false;  // panel J was factored on the side stream
-  for (int J = 0; J < ncols; J += nb) {
-    const int w = min(nb, ncols - J);
+  const int pc = min(m, ncols);  // columns that are pivoted
+  for (int J = 0; J < pc; J += nb) {
+    const int w = min(nb, pc - J);
     const int slot = (J / nb) & 1;
     int32_t *sl = ws.swap_list + slot * LU_SWAP_LIST;
     if (panel_pending) {
@@ -405,13 +409,13 @@ cudaError_t enqueue_lu(int k, int m, int ncols, MatView A, int32_t *d_swaps,
         return e;
     }
     const int rest_r = m - J - w, rest_c = ncols - J - w;
-    const int J2 = J + w, w2 = min(nb, max(0, ncols - J2));
+    const int J2 = J + w, w2 = min(nb, max(0, pc - J2));
     // exchanges on every other column, U12 of the trailing columns
     if ((e = lu_swap_trsm(k, A, J, w, 0, J, J2, ncols, sl, ws.status, s)) !=
         cudaSuccess)
       return e;
     if (rest_c <= 0 || rest_r <= 0) continue;
-    if (!ahead) {
+    if (!ahead || w2 == 0) {
       if ((e = lu_update(k, rest_r, rest_c, w, sub(A, J2, J), sub(A, J, J2),
                          sub(A, J2, J2), ws.status, s)) != cudaSuccess)
         return e;
@@ -588,7 +592,7 @@ cudaError_t lu_factor(int k, int m, int ncols, MatView A, int32_t *d_swaps,
       e = cudaGraphInstantiate(&exec, graph, 0);
       cudaGraphDestroy(graph);
       if (e != cudaSuccess) return e;
-      if (gc.entries.size() >= 16) {
+      if (gc.entries.size() >= 512) {  // tall blocks: one shape per panel
         cudaGraphExecDestroy(gc.entries.front().exec);
         gc.entries.erase(gc.entries.begin());
       }

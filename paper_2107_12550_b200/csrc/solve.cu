@@ -408,7 +408,42 @@ cudaError_t solve_k(int n, MatView LU, const int32_t *perm, const double *b,
                      sw.words, sw.next_seq(), tb);
 }
 
+template <int K>
+cudaError_t back_k(int n, MatView LU, double *x, SolveWork &sw,
+                   cudaStream_t s) {
+  const size_t smem = sweep_smem<K>();
+  auto bk = sweep_kernel<K, true>;
+  static bool configured = false;
+  cudaError_t e;
+  if (!configured) {
+    if ((e = cudaFuncSetAttribute(
+             bk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+      return e;
+    configured = true;
+  }
+  const int nblk = (n + SB - 1) / SB;
+  if ((e = sw.ensure(n)) != cudaSuccess) return e;
+  u64 *tb = sw.trace ? sw.trace + (int64_t)8 * nblk : nullptr;
+  return launch_coop(bk, coop_grid(bk, smem, nblk), smem, s, n, LU, x,
+                     sw.words, sw.next_seq(), tb);
+}
+
 }  // namespace
+
+cudaError_t lu_solve_back(int k, int n, MatView LU, double *x, SolveWork &sw,
+                          cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  prof_begin(PROF_SOLVE, s);
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (k) {
+    case 2: e = back_k<2>(n, LU, x, sw, s); break;
+    case 3: e = back_k<3>(n, LU, x, sw, s); break;
+    case 4: e = back_k<4>(n, LU, x, sw, s); break;
+  }
+  prof_end(PROF_SOLVE, s);
+  return e;
+}
 
 cudaError_t SolveWork::ensure(int64_t rows) {
   if (rows <= cap) return cudaSuccess;

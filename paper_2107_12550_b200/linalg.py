@@ -17,6 +17,7 @@ signature compatibility; there is exactly one execution path.  BigFloat
 (long-precision) containers live in ``longfloat`` and stay on the host.
 """
 
+import ctypes
 import math
 
 import numpy as np
@@ -316,6 +317,13 @@ class DeviceMatrix:
     def copy_from(self, other):
         nat.check(nat.lib().mpcore_copy(other.handle, self.handle), "copy")
 
+    def device_ptr(self):
+        """Address of component plane 0, element 0 (planar, row-major)."""
+        p = ctypes.c_uint64()
+        nat.check(nat.lib().mpcore_object_device_ptr(self.handle,
+                                                     ctypes.byref(p)), "ptr")
+        return p.value
+
     def lu_factor(self, nb=0):
         """In-place factorisation -> (PivotHandle)."""
         st, piv, step = nat.lu_factor(self.handle, nb)
@@ -345,6 +353,13 @@ class DeviceVector:
     def upload(self, planes):
         nat.set_planes(self.handle, planes)
 
+    def device_ptr(self):
+        """Address of component plane 0, element 0 (planar)."""
+        p = ctypes.c_uint64()
+        nat.check(nat.lib().mpcore_object_device_ptr(self.handle,
+                                                     ctypes.byref(p)), "ptr")
+        return p.value
+
     def download(self, out=None):
         return nat.get_planes(self.handle, (self.k, self.n), out)
 
@@ -373,6 +388,24 @@ class PivotHandle:
 def device_solve(lu, piv, b, x):
     nat.check(nat.lib().mpcore_lu_solve(lu.handle, piv.handle, b.handle,
                                         x.handle), "lu_solve")
+
+
+def device_solve_system(A, b, x, nb=0):
+    """x = A^-1 b in one call (mpcore_solve_system): A is left holding its
+    LU factors and the PivotHandle is returned, exactly as
+    ``A.lu_factor(nb)`` + ``device_solve`` would leave them; b rides along
+    the factorisation as an extra column (its forward substitution), so only
+    the back substitution runs afterwards."""
+    h = ctypes.c_uint64()
+    step = ctypes.c_int32(-1)
+    st = nat.lib().mpcore_solve_system(A.handle, b.handle, x.handle, int(nb),
+                                       ctypes.byref(h), ctypes.byref(step))
+    if st == nat.SINGULAR:
+        raise SingularMatrixError(
+            "no nonzero pivot at elimination step %d" % step.value,
+            step=step.value)
+    nat.check(st, "solve_system")
+    return PivotHandle(h.value, A.rows)
 
 
 # ---------------------------------------------------------------------------

@@ -10,7 +10,8 @@ import pytest
 import oracle
 from oracle import gen
 from paper_2107_12550_b200 import _native as nat
-from paper_2107_12550_b200.linalg import DeviceMatrix, DeviceVector, device_solve
+from paper_2107_12550_b200.linalg import (DeviceMatrix, DeviceVector,
+                                          device_solve, device_solve_system)
 
 pytestmark = pytest.mark.gpu
 
@@ -32,6 +33,14 @@ def test_bench_workload_bitwise(k, n, seed):
     x = DeviceVector(k, n)
     device_solve(A0, piv, b, x)
     lu_ref, sw_ref = oracle.lu(A)
+    x_ref = oracle.solve(lu_ref, sw_ref, bh)
     assert np.asarray(piv.swaps()).tobytes() == sw_ref.tobytes()
     assert A0.download().tobytes() == lu_ref.tobytes()
-    assert x.download().tobytes() == oracle.solve(lu_ref, sw_ref, bh).tobytes()
+    assert x.download().tobytes() == x_ref.tobytes()
+    # the bench's one-call path (b as an extra column of the LU)
+    A1 = DeviceMatrix.from_planes(A)
+    x1 = DeviceVector(k, n)
+    piv1 = device_solve_system(A1, b, x1)
+    assert np.asarray(piv1.swaps()).tobytes() == sw_ref.tobytes()
+    assert A1.download().tobytes() == lu_ref.tobytes()
+    assert x1.download().tobytes() == x_ref.tobytes()
