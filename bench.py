@@ -37,6 +37,9 @@ MADD_INSTR = {2: 29, 3: 214, 4: 326}
 REF_MADD_INSTR = {2: 29, 3: 264, 4: 376}
 MUL_INSTR = {2: 9, 3: 133, 4: 181}
 DIV_INSTR = {2: 113, 3: 491, 4: 1165}
+# DFMA per op (one per two_prod; each DFMA is 2 flops): flop-weighted rates
+MADD_DFMA = {2: 1, 3: 6, 4: 6}
+MUL_DFMA = {2: 1, 3: 6, 4: 6}
 SEED = 210712550 + 2                      # config index 2
 
 
@@ -49,7 +52,9 @@ def work_counts(n, k):
     sv_divs = n
     instr = ((lu_madds + sv_madds) * MADD_INSTR[k] + lu_muls * MUL_INSTR[k]
              + (lu_divs + sv_divs) * DIV_INSTR[k])
-    return dict(lu_madds=lu_madds, sv_madds=sv_madds, instr=instr)
+    flops = instr + (lu_madds + sv_madds) * MADD_DFMA[k] + lu_muls * MUL_DFMA[k]
+    return dict(lu_madds=lu_madds, sv_madds=sv_madds, instr=instr,
+                flops=flops)
 
 
 def update_madds(n, nb):
@@ -341,6 +346,20 @@ def run_ours(args):
                             "(profiles/r01_traffic.json; its algorithmic "
                             "bytes are listed there)",
             "whole_step_frac": overall_rate / peak if peak else None,
+            # flop-weighted (DFMA = 2 flops) against the DFMA issue peak
+            # (the datasheet's FP64 TFLOP/s figure is 2 x the DFMA rate)
+            "fp64_tflops": wc["flops"] / (ms * 1e-3) / 1e12,
+            "fp64_tflops_peak": 2 * peak_fma / 1e12,
+            "flop_frac": (wc["flops"] / (ms * 1e-3)) / (2 * peak_fma)
+                         if peak_fma else None,
+            # the latency-bound kernels against HBM
+            "solve_hbm_gbs": (k * 8 * n * n / 2 + 4 * k * 8 * n)
+                             / (prof["solve"][0] / args.steps * 1e-3) / 1e9
+                             if prof["solve"][1] else None,
+            "panel_hbm_gbs": (2 * k * 8 * n * (n + 32) / 2)
+                             / (prof["panel"][0] / args.steps * 1e-3) / 1e9
+                             if prof["panel"][1] else None,
+            "hbm_peak_gbs": 6553.3,
         },
         "kernels_ms_per_step": {s: v[0] / args.steps for s, v in prof.items()
                                 if v[1]},

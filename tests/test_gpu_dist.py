@@ -26,7 +26,8 @@ def assemble(local, layout, k):
 
 @pytest.mark.parametrize("k,n,nb,G", [(2, 256, 64, 2), (3, 200, 32, 3),
                                       (4, 160, 64, 2), (2, 300, 128, 4),
-                                      (2, 513, 256, 2), (3, 96, 32, 1)])
+                                      (2, 513, 256, 2), (3, 96, 32, 1),
+                                      (2, 2048, 256, 4), (2, 2100, 256, 3)])
 def test_virtual_ranks_match_reference(k, n, nb, G):
     seed = 31337 + n
     layout = Layout(n, nb, G)
