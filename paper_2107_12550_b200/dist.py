@@ -76,6 +76,12 @@ class LocalComm:
     def broadcast(self, buf, root):
         return buf
 
+    def ibroadcast(self, buf, root):
+        return None
+
+    def wait(self, handle):
+        pass
+
     def barrier(self):
         pass
 
@@ -94,6 +100,21 @@ class TorchComm:
             import torch
             torch.cuda.current_stream().synchronize()
         return buf
+
+    def ibroadcast(self, buf, root):
+        """Start a broadcast (NCCL: on its own stream, so the sender's next
+        kernels overlap it); wait() before reading the buffer."""
+        return (self.dist.broadcast(buf, src=root, group=self.group,
+                                    async_op=True), buf)
+
+    def wait(self, handle):
+        if handle is None:
+            return
+        work, buf = handle
+        work.wait()
+        if buf.is_cuda:
+            import torch
+            torch.cuda.current_stream().synchronize()
 
     def barrier(self):
         self.dist.barrier(group=self.group)
@@ -213,48 +234,114 @@ def _local_ranges(layout, rank, P):
     return [(0, off), (off + w, lc - off - w)]
 
 
-def dist_lu_factor(backend, comm, layout, local):
+def dist_lu_factor(backend, comm, layout, local, lookahead=True):
     """Factor the distributed matrix in place.
 
     local: {rank: local block (backend storage)} for the ranks this process
     serves (all of them under LocalComm).  Returns the global swap list
     (swaps[j] = r, the reference's PivotRecord.swaps, linalg.py:348-354).
     Raises SingularMatrixError(step) on every rank alike.
+
+    Look-ahead: while applying panel P, the owner of panel
+    P+1 first brings that block up to date (exchanges, U12, update of its
+    columns only), factors it and starts its broadcast, and only then runs
+    the bulk of its update for P -- so the next panel travels while every
+    rank updates.  Only the order across column blocks changes; each
+    element's chain is the same, so the result is identical either way.
     """
     n, G = layout.n, layout.world
-    k = backend.k
+    nbk = layout.nblocks
     swaps_all = np.zeros(n, dtype=np.int32)
-    buf = backend.alloc(n, layout.nb)
-    ibuf = backend.int_buffer(layout.nb + 1)
-    for P in range(layout.nblocks):
+    bufs = [backend.alloc(n, layout.nb), backend.alloc(n, layout.nb)]
+    ibufs = [backend.int_buffer(layout.nb + 1),
+             backend.int_buffer(layout.nb + 1)]
+
+    def factor_pack(P, slot):
+        """Owner of P: factor its block, pack it, stage pivots + status."""
         J, w, owner = P * layout.nb, layout.width(P), layout.owner(P)
+        M = local[owner]
+        off = layout.local_offset(owner, P)
         status = np.zeros(layout.nb + 1, dtype=np.int32)
-        if owner in local:
-            M = local[owner]
-            off = layout.local_offset(owner, P)
-            try:
-                sw = backend.lu_block(M, J, off, w)
-                status[:w] = sw
-                status[layout.nb] = -1
-            except SingularMatrixError as e:
-                status[layout.nb] = e.step
-            backend.pack(M, J, off, w, buf)
-        backend.ints_from_host(ibuf, status)
-        comm.broadcast(ibuf, owner)            # pivots (+ singular flag)
-        status = backend.ints_to_host(ibuf)
+        try:
+            status[:w] = backend.lu_block(M, J, off, w)
+            status[layout.nb] = -1
+        except SingularMatrixError as e:
+            status[layout.nb] = e.step
+        backend.pack(M, J, off, w, bufs[slot])
+        backend.ints_from_host(ibufs[slot], status)
+
+    def send(P, slot):
+        """Every rank, in panel order: start P's broadcasts."""
+        owner = layout.owner(P)
+        return (comm.ibroadcast(ibufs[slot], owner),
+                comm.ibroadcast(bufs[slot], owner))
+
+    def update(M, rank, P, sw, buf, c0, nc, exchange_ranges):
+        """Panel P applied to local columns: exchanges on the given ranges,
+        then U12 and the trailing update on [c0, c0 + nc)."""
+        J, w = P * layout.nb, layout.width(P)
+        for a, m in exchange_ranges:
+            backend.laswp(M, a, m, J, sw)
+        if nc > 0:
+            backend.trsm(buf, w, M, J, c0, nc)
+            backend.gemm_update(buf, w, M, J, c0, nc)
+
+    if layout.owner(0) in local:
+        factor_pack(0, 0)
+    pending = send(0, 0)
+    for P in range(nbk):
+        J, w = P * layout.nb, layout.width(P)
+        slot = P % 2
+        comm.wait(pending[0])
+        status = backend.ints_to_host(ibufs[slot])
         if status[layout.nb] >= 0:
             raise SingularMatrixError(
                 "no nonzero pivot at elimination step %d" % status[layout.nb],
                 step=int(status[layout.nb]))
-        comm.broadcast(buf, owner)             # factored panel L21 / L11 / U11
+        comm.wait(pending[1])
+        buf = bufs[slot]
         sw = status[:w].copy()
         swaps_all[J:J + w] = sw
+        nxt = P + 1 < nbk
+        # (one rank has nobody to overlap with: keep the launches fewer)
+        ahead = lookahead and nxt and G > 1
+        if ahead:
+            # the next panel's owner: that block first, then factor + send
+            o1 = layout.owner(P + 1)
+            if o1 in local:
+                M = local[o1]
+                off1, w1 = layout.local_offset(o1, P + 1), layout.width(P + 1)
+                update(M, o1, P, sw, buf, off1, w1, [(off1, w1)])
+                factor_pack(P + 1, 1 - slot)
+            pending = send(P + 1, 1 - slot)
         for rank, M in local.items():
-            for c0, nc in _local_ranges(layout, rank, P):
-                backend.laswp(M, c0, nc, J, sw)
             t0 = layout.trailing_start(rank, P)
             nt = layout.local_cols(rank) - t0
-            if nt > 0:
-                backend.trsm(buf, w, M, J, t0, nt)
-                backend.gemm_update(buf, w, M, J, t0, nt)
+            ranges = _local_ranges(layout, rank, P)
+            if ahead and rank == layout.owner(P + 1):
+                # block P+1 (the first trailing block) is already done
+                w1 = layout.width(P + 1)
+                ranges = _split_out(ranges, t0, w1)
+                t0, nt = t0 + w1, nt - w1
+            update(M, rank, P, sw, buf, t0, nt, ranges)
+        if nxt and not ahead:
+            if layout.owner(P + 1) in local:
+                factor_pack(P + 1, 1 - slot)
+            pending = send(P + 1, 1 - slot)
     return swaps_all
+
+
+def _split_out(ranges, a0, m0):
+    """Column ranges minus [a0, a0 + m0)."""
+    out = []
+    for a, m in ranges:
+        b = a + m
+        if b <= a0 or a >= a0 + m0:
+            if m > 0:
+                out.append((a, m))
+            continue
+        if a < a0:
+            out.append((a, a0 - a))
+        if b > a0 + m0:
+            out.append((a0 + m0, b - a0 - m0))
+    return out

@@ -112,16 +112,17 @@ def assemble(local, layout):
     return full
 
 
+@pytest.mark.parametrize("lookahead", [True, False])
 @pytest.mark.parametrize("k,n,nb,G", [(2, 96, 16, 1), (2, 96, 16, 2),
                                       (3, 80, 32, 3), (4, 70, 16, 2),
                                       (2, 130, 32, 4), (3, 64, 64, 2)])
-def test_local_world_matches_reference_lu(k, n, nb, G):
+def test_local_world_matches_reference_lu(k, n, nb, G, lookahead):
     A = gen.planes(k, (n, n), 0, n, 4242 + n)
     lu_ref, sw_ref = oracle.lu(A)
     layout = Layout(n, nb, G)
     be = OracleBackend(k)
     local = local_blocks(A, layout, range(G), be)
-    swaps = dist_lu_factor(be, LocalComm(), layout, local)
+    swaps = dist_lu_factor(be, LocalComm(), layout, local, lookahead)
     assert swaps.tobytes() == sw_ref.tobytes()
     assert assemble(local, layout).tobytes() == lu_ref.tobytes()
 
@@ -163,7 +164,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, k, n, nb, out_dir):
+def _worker(rank, world, port, k, n, nb, out_dir, lookahead=True):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -173,7 +174,7 @@ def _worker(rank, world, port, k, n, nb, out_dir):
         layout = Layout(n, nb, world)
         be = OracleBackend(k)
         local = local_blocks(A, layout, [rank], be)
-        swaps = dist_lu_factor(be, TorchComm(), layout, local)
+        swaps = dist_lu_factor(be, TorchComm(), layout, local, lookahead)
         np.save(os.path.join(out_dir, "rank%d.npy" % rank), local[rank].numpy())
         np.save(os.path.join(out_dir, "swaps%d.npy" % rank), swaps)
         dist.barrier()
@@ -181,11 +182,13 @@ def _worker(rank, world, port, k, n, nb, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("k,n,nb", [(2, 100, 16), (3, 72, 32)])
-def test_gloo_world2_matches_reference_lu(tmp_path, k, n, nb):
+@pytest.mark.parametrize("k,n,nb,world,lookahead",
+                         [(2, 100, 16, 2, True), (3, 72, 32, 2, False),
+                          (2, 90, 16, 3, True)])
+def test_gloo_world_matches_reference_lu(tmp_path, k, n, nb, world, lookahead):
     import torch.multiprocessing as mp
-    world = 2
-    mp.spawn(_worker, args=(world, _free_port(), k, n, nb, str(tmp_path)),
+    mp.spawn(_worker, args=(world, _free_port(), k, n, nb, str(tmp_path),
+                            lookahead),
              nprocs=world, join=True)
     A = gen.planes(k, (n, n), 0, n, 99 + n)
     lu_ref, sw_ref = oracle.lu(A)
