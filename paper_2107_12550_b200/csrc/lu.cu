@@ -170,19 +170,25 @@ trsm_kernel(MatView L11, MatView U12, int w, int ncols,
 // second sweep; U12 = L11^-1 A12 runs in registers, x_t broadcast by
 // shuffles (no CTA barrier per step).  Columns [c2, c3) get both, [c0, c1)
 // (the already factored L columns) only the exchanges.
-template <int K>
+template <int K, int LPC>
 __global__ void __launch_bounds__(128)
 swap_trsm_kernel(MatView A, int J, int w, int c0, int c1, int c2, int c3,
                  const int32_t *__restrict__ swap_list,
                  const int32_t *__restrict__ status) {
+  // LPC lanes per column: 32 (one row per lane) or 16 (rows r and 31-r per
+  // lane -- the triangle's shrinking work stays balanced, so a warp does
+  // 46 madd steps for two columns instead of 62)
+  constexpr int CPW = 32 / LPC, CPB = 4 * CPW, NE = 2 * LU_MAX_W / LPC;
   if (status[0] >= 0) return;
   __shared__ int cur[2 * LU_MAX_W], src[2 * LU_MAX_W], rsrc[LU_MAX_W];
   __shared__ double Ls[K][LU_MAX_W][LU_MAX_W + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nright = (c3 - c2 + 3) / 4;
+  const int sl = lane % LPC, gbase = lane - sl;   // sub-lane, group's lane 0
+  const int nright = (c3 - c2 + CPB - 1) / CPB;
   const bool right = (int)blockIdx.x < nright;
-  const int col = right ? c2 + blockIdx.x * 4 + warp
-                        : c0 + (blockIdx.x - nright) * 4 + warp;
+  const int cslot = warp * CPW + lane / LPC;
+  const int col = right ? c2 + blockIdx.x * CPB + cslot
+                        : c0 + (blockIdx.x - nright) * CPB + cslot;
   const int cend = right ? c3 : c1;
   const int cnt = swap_list[4 * LU_MAX_W];
   if (tid < 2 * LU_MAX_W) {
@@ -206,46 +212,84 @@ swap_trsm_kernel(MatView A, int J, int w, int c0, int c1, int c2, int c3,
   // the post-exchange source of each panel row (cur entries are distinct)
   if (right && tid < cnt && cur[tid] < J + w) rsrc[cur[tid] - J] = src[tid];
   __syncthreads();
-  if (col >= cend) return;
+  const bool live = col < cend;   // (no early return: shuffles below)
   const int64_t ld = A.ld;
-  double *pc = A.p + col;
-  // exchange entries (lane, lane + 32); with U12 the panel rows are written
-  // by the solve below, so only destinations below the panel are kept here
-  const int i0 = lane, i1 = lane + 32;
-  const bool e0 = i0 < cnt && (!right || cur[i0] >= J + w);
-  const bool e1 = i1 < cnt && (!right || cur[i1] >= J + w);
-  double v0[K], v1[K], u[K];
+  double *pc = A.p + (live ? col : c2);
+  // exchange entries sl + LPC*q; with U12 the panel rows are written by the
+  // solve below, so only destinations below the panel are kept here
+  bool ex[NE];
+  double v[NE][K];
+#pragma unroll
+  for (int q = 0; q < NE; ++q) {
+    const int i = sl + LPC * q;
+    ex[q] = live && i < cnt && (!right || cur[i] >= J + w);
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      v[q][k] = ex[q] ? pc[k * A.plane + (int64_t)src[i] * ld] : 0.0;
+  }
+  // rows of this lane: ra = sl, rb = 31 - sl (LPC = 16 only)
+  const int ra = sl, rb = LU_MAX_W - 1 - sl;
+  double ua[K], ub[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    v0[k] = e0 ? pc[k * A.plane + (int64_t)src[i0] * ld] : 0.0;
-    v1[k] = e1 ? pc[k * A.plane + (int64_t)src[i1] * ld] : 0.0;
-    u[k] = (right && lane < w) ? pc[k * A.plane + (int64_t)rsrc[lane] * ld]
-                               : 0.0;
+    ua[k] = (live && right && ra < w) ? pc[k * A.plane + (int64_t)rsrc[ra] * ld]
+                                      : 0.0;
+    ub[k] = (LPC == 16 && live && right && rb < w)
+                ? pc[k * A.plane + (int64_t)rsrc[rb] * ld]
+                : 0.0;
   }
   __syncwarp();
   if (right) {
     for (int t = 0; t + 1 < w; ++t) {
-      double ut[K], l[K], o[K];
+      // row t lives in slot a of sub-lane t (t < LPC), else in slot b of
+      // sub-lane 31 - t
+      const bool in_a = t < LPC;
+      const int srcl = gbase + (in_a ? t : LU_MAX_W - 1 - t);
+      double ut[K];
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        ut[k] = __shfl_sync(0xffffffffu, u[k], t);
-        l[k] = Ls[k][lane][t];
-        o[k] = u[k];
+      for (int k = 0; k < K; ++k)
+        ut[k] = __shfl_sync(0xffffffffu, in_a ? ua[k] : ub[k], srcl);
+      if (t < LPC - 1) {  // some row of slot a is still below t
+        double l[K], o[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          l[k] = Ls[k][ra][t];
+          o[k] = ua[k];
+        }
+        mc::madd<K>(o, l, ut);
+        const bool upd = ra > t && ra < w;
+#pragma unroll
+        for (int k = 0; k < K; ++k) ua[k] = upd ? o[k] : ua[k];
       }
-      mc::madd<K>(o, l, ut);
-      const bool upd = lane > t && lane < w;
+      if (LPC == 16) {
+        double l[K], o[K];
 #pragma unroll
-      for (int k = 0; k < K; ++k) u[k] = upd ? o[k] : u[k];
+        for (int k = 0; k < K; ++k) {
+          l[k] = Ls[k][rb][t];
+          o[k] = ub[k];
+        }
+        mc::madd<K>(o, l, ut);
+        const bool upd = rb > t && rb < w;
+#pragma unroll
+        for (int k = 0; k < K; ++k) ub[k] = upd ? o[k] : ub[k];
+      }
     }
-    if (lane < w) {
+    if (live && ra < w) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) pc[k * A.plane + (int64_t)(J + lane) * ld] = u[k];
+      for (int k = 0; k < K; ++k) pc[k * A.plane + (int64_t)(J + ra) * ld] = ua[k];
+    }
+    if (LPC == 16 && live && rb < w) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) pc[k * A.plane + (int64_t)(J + rb) * ld] = ub[k];
     }
   }
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    if (e0) pc[k * A.plane + (int64_t)cur[i0] * ld] = v0[k];
-    if (e1) pc[k * A.plane + (int64_t)cur[i1] * ld] = v1[k];
+  for (int q = 0; q < NE; ++q) {
+    if (ex[q]) {
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        pc[k * A.plane + (int64_t)cur[sl + LPC * q] * ld] = v[q][k];
+    }
   }
 }
 
@@ -363,13 +407,15 @@ struct GraphCache {
 cudaError_t lu_swap_trsm(int k, MatView A, int J, int w, int c0, int c1,
                          int c2, int c3, const int32_t *swap_list,
                          const int32_t *status, cudaStream_t s) {
+  // CTAs of 4 warps: 4 columns (DD, a lane per row) or 8 (TD/QD)
   const int nl = (max(0, c1 - c0) + 3) / 4, nr = (max(0, c3 - c2) + 3) / 4;
+  const int nl2 = (max(0, c1 - c0) + 7) / 8, nr2 = (max(0, c3 - c2) + 7) / 8;
   if (nl + nr == 0) return cudaSuccess;
   prof_begin(PROF_TRSM, s);
   switch (k) {
-    case 2: swap_trsm_kernel<2><<<nl + nr, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status); break;
-    case 3: swap_trsm_kernel<3><<<nl + nr, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status); break;
-    case 4: swap_trsm_kernel<4><<<nl + nr, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status); break;
+    case 2: swap_trsm_kernel<2, 32><<<nl + nr, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status); break;
+    case 3: swap_trsm_kernel<3, 16><<<nl2 + nr2, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status); break;
+    case 4: swap_trsm_kernel<4, 16><<<nl2 + nr2, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status); break;
     default: return cudaErrorInvalidValue;
   }
   prof_end(PROF_TRSM, s);
