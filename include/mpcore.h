@@ -247,6 +247,11 @@ int32_t mpcore_debug_panel_trace(uint64_t *out_ns, int64_t cap);
  * (MPCORE_TRACE_SOLVE set): [forward, backward][blocks][4] = start, completed
  * source blocks added, critical source block done, diagonal done */
 int32_t mpcore_debug_solve_trace(uint64_t *out_ns, int64_t cap);
+/* diagnostics: the refinement loop's fixed-width long arithmetic against
+ * the generic big-integer path on random operands at precision prec
+ * (<= 640); host only */
+int32_t mpcore_debug_longfloat_selftest(int64_t iters, uint64_t seed,
+                                        int32_t prec, int64_t *mismatches);
 /* diagnostics: timeline of the profiled launches since mpcore_prof_reset,
  * (slot, start us, end us) per launch in enqueue order */
 int32_t mpcore_debug_timeline(double *out, int64_t cap, int64_t *count);

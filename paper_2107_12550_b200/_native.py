@@ -84,6 +84,8 @@ _PROTOS = {
     "mpcore_report_timings": (_i32, [_u64, ctypes.POINTER(ctypes.c_double),
                                      _i32, ctypes.POINTER(_i32)]),
     "mpcore_debug_solve_trace": (_i32, [ctypes.POINTER(_u64), _i64]),
+    "mpcore_debug_longfloat_selftest": (_i32, [_i64, _u64, _i32,
+                                               ctypes.POINTER(_i64)]),
     "mpcore_debug_timeline": (_i32, [ctypes.POINTER(ctypes.c_double), _i64,
                                      ctypes.POINTER(_i64)]),
     # device-pointer building blocks (dist.py)

@@ -1198,6 +1198,13 @@ int32_t mpcore_debug_panel_trace(uint64_t *out_ns, int64_t cap) {
   return MPCORE_OK;
 }
 
+int32_t mpcore_debug_longfloat_selftest(int64_t iters, uint64_t seed,
+                                        int32_t prec, int64_t *mismatches) {
+  if (!mismatches) return MPCORE_BAD_DIMENSION;
+  *mismatches = mpr::longfloat_selftest(iters, seed, prec);
+  return *mismatches < 0 ? MPCORE_BAD_DIMENSION : MPCORE_OK;
+}
+
 int32_t mpcore_debug_solve_trace(uint64_t *out_ns, int64_t cap) {
   DevLock L;
   if (L.st) return L.st;

@@ -8,6 +8,8 @@
 // ShortSolver (cabi.cu).
 #include "refine_host.h"
 
+#include "fastfloat.h"
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -362,11 +364,29 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
   };
   std::vector<BF> x;
   lift(x_pl, x);
-  // ||A||_F, row-major accumulation (linalg.py:692-700)
-  // (the squares are independent: formed on all threads, then summed in
-  // the reference's order)
+  // ||A||_F, row-major accumulation (linalg.py:692-700); the squares are
+  // independent: formed on all threads, then summed in the reference's order
+  const bool fast = p <= 64 * ff::NL;   // fixed-width path (fastfloat.h)
+  const int pi = (int)p;
+  std::vector<ff::F> Af, Bf;
+  if (fast) {
+    Af.resize(Avals.size());
+    par_rows(Avals.size(), threads, [&](size_t a, size_t b) {
+      for (size_t e = a; e < b; ++e) Af[e] = ff::from_bf(Avals[e], pi);
+    });
+    Bf.resize(n);
+    for (int i = 0; i < n; ++i) Bf[i] = ff::from_bf(Bvals[i], pi);
+  }
   BF a_fro;
-  {
+  if (fast) {
+    std::vector<ff::F> sq(Af.size());
+    par_rows(Af.size(), threads, [&](size_t a, size_t b) {
+      for (size_t e = a; e < b; ++e) sq[e] = ff::mul(Af[e], Af[e], pi);
+    });
+    ff::F acc;
+    for (const ff::F &v : sq) acc = ff::add(acc, v, pi);
+    a_fro = lf_sqrt(ff::to_bf(acc), p);
+  } else {
     std::vector<BF> sq(Avals.size());
     par_rows(Avals.size(), threads, [&](size_t a, size_t b) {
       for (size_t e = a; e < b; ++e) sq[e] = lf_mul(Avals[e], Avals[e], p);
@@ -378,25 +398,52 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
   const BF one = from_int(1, p);
   // check_stop threshold factor sqrt(n) * rtol * a_fro, left to right
   std::vector<BF> res(n), work(n), z;
+  std::vector<ff::F> xf, resf;
+  auto norm2_f = [&](const std::vector<ff::F> &v) {
+    ff::F acc;
+    for (const ff::F &s : v) acc = ff::add(acc, ff::mul(s, s, pi), pi);
+    return lf_sqrt(ff::to_bf(acc), p);
+  };
   std::string reason = "max_iter";
   int corrections = 0;
   out.residuals.clear();
   for (int it = 0; it < max_iter; ++it) {
     // res = b - A x  (scalar mat_vec order per row, linalg.py:566-574)
     const auto ta = Clock::now();
-    par_rows((size_t)n, threads, [&](size_t r0, size_t r1) {
-      for (size_t i = r0; i < r1; ++i) {
-        BF acc;
-        const BF *row = &Avals[i * n];
-        for (int j = 0; j < n; ++j) acc = lf_add(acc, lf_mul(row[j], x[j], p), p);
-        res[i] = lf_sub(Bvals[i], acc, p);
-      }
-    });
-    t_res += secs(ta, Clock::now());
-    BF res_norm = norm2(res, p);
+    BF res_norm, x_norm;
+    if (fast) {
+      xf.resize(n);
+      for (int i = 0; i < n; ++i) xf[i] = ff::from_bf(x[i], pi);
+      resf.resize(n);
+      par_rows((size_t)n, threads, [&](size_t r0, size_t r1) {
+        for (size_t i = r0; i < r1; ++i) {
+          ff::F acc;
+          const ff::F *row = &Af[i * n];
+          for (int j = 0; j < n; ++j)
+            acc = ff::add(acc, ff::mul(row[j], xf[j], pi), pi);
+          resf[i] = ff::add(Bf[i], ff::neg(acc), pi);
+        }
+      });
+      t_res += secs(ta, Clock::now());
+      for (int i = 0; i < n; ++i) res[i] = ff::to_bf(resf[i]);
+      res_norm = norm2_f(resf);
+      x_norm = norm2_f(xf);
+    } else {
+      par_rows((size_t)n, threads, [&](size_t r0, size_t r1) {
+        for (size_t i = r0; i < r1; ++i) {
+          BF acc;
+          const BF *row = &Avals[i * n];
+          for (int j = 0; j < n; ++j)
+            acc = lf_add(acc, lf_mul(row[j], x[j], p), p);
+          res[i] = lf_sub(Bvals[i], acc, p);
+        }
+      });
+      t_res += secs(ta, Clock::now());
+      res_norm = norm2(res, p);
+      x_norm = norm2(x, p);
+    }
     out.residuals.push_back(res_norm);
     if (res_norm.sign == 0) { reason = "converged"; break; }
-    BF x_norm = norm2(x, p);
     BF t = lf_sqrt(from_int(n, p), p);
     t = lf_mul(t, rtol, p);
     t = lf_mul(t, a_fro, p);
@@ -427,6 +474,58 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
   // convert, factor, refinement loop (incl. first solve), residuals, solves
   out.timings = {secs(t0, t1), secs(t1, t2), secs(t2, t3), t_res, t_solve};
   return 0;
+}
+
+// fastfloat.h vs the generic path on random operands (diagnostics / tests)
+int64_t longfloat_selftest(int64_t iters, uint64_t seed, int p) {
+  if (p < 2 || p > 64 * ff::NL) return -1;
+  uint64_t z = seed;
+  auto rnd = [&]() {
+    z += 0x9E3779B97F4A7C15ull;
+    uint64_t x = z;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+  };
+  auto rand_bf = [&](int64_t e_center) {
+    // random p-bit (or shorter) mantissa, exponent near e_center
+    bn::BF v;
+    const int bits = 1 + (int)(rnd() % (uint64_t)p);
+    bn::UBig m;
+    for (int b = 0; b < bits; b += 32) m.w.push_back((uint32_t)rnd());
+    m = m.shr((int64_t)m.w.size() * 32 - bits);
+    if (m.w.empty()) m = bn::UBig(1);
+    if (!m.bit(bits - 1)) m = bn::UBig::add(m.shl(0), bn::UBig(1).shl(bits - 1));
+    if (rnd() % 8 == 0) {  // runs of ones: carries through every limb
+      m = bn::UBig(1).shl(bits);
+      m = bn::UBig::sub(m, bn::UBig(1 + rnd() % 3));
+    }
+    v.sign = (rnd() & 1) ? 1 : -1;
+    v.man = m;
+    v.exp = e_center - bits + (int64_t)(rnd() % 7) - 3;
+    v.man.trim();
+    return v;
+  };
+  int64_t bad = 0;
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t gap_kind = rnd() % 6;
+    int64_t gap = gap_kind == 0 ? 0
+                  : gap_kind == 1 ? (int64_t)(rnd() % 4)
+                  : gap_kind == 2 ? (int64_t)(rnd() % (uint64_t)(p + 8))
+                  : gap_kind == 3 ? p + (int64_t)(rnd() % 6) - 3
+                  : (int64_t)(rnd() % 3000);
+    BF a = lf_round(rand_bf(0), p), b = lf_round(rand_bf(-gap), p);
+    if (rnd() % 16 == 0) b = bn::neg(a);          // exact cancellation
+    if (rnd() % 16 == 1) b = lf_round(bn::neg(a), p - 1 > 1 ? p - 1 : p);
+    const ff::F fa = ff::from_bf(a, p), fb = ff::from_bf(b, p);
+    const BF s_ref = lf_add(a, b, p), s = ff::to_bf(ff::add(fa, fb, p));
+    const BF d_ref = lf_sub(a, b, p), d = ff::to_bf(ff::add(fa, ff::neg(fb), p));
+    const BF m_ref = lf_mul(a, b, p), mm = ff::to_bf(ff::mul(fa, fb, p));
+    if (lf_cmp(s, s_ref) != 0 || s.sign != s_ref.sign) ++bad;
+    if (lf_cmp(d, d_ref) != 0 || d.sign != d_ref.sign) ++bad;
+    if (lf_cmp(mm, m_ref) != 0 || mm.sign != m_ref.sign) ++bad;
+  }
+  return bad;
 }
 
 int refine_files(const char *a_path, const char *b_path, int short_k,

@@ -48,6 +48,10 @@ int refine_core(std::vector<bn::BF> &A, std::vector<bn::BF> &B, int n,
                 int max_iter, int threads, ShortSolver &short_side, Report &out,
                 std::string &err);
 
+// fastfloat.h against the generic big-integer path: mismatches over iters
+// random operand pairs at precision p (-1: p out of the fixed-width range)
+int64_t longfloat_selftest(int64_t iters, uint64_t seed, int p);
+
 // bf_format_hex (bigfloat.py:524-537) and a .mpmat writer (matfile.py
 // layout: header "mpmat rows cols bf bits", one row per line)
 std::string format_hex(const bn::BF &v);

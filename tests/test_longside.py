@@ -103,3 +103,15 @@ def test_refinement_matches_reference(monkeypatch, idx):
     assert rep.stop_reason == case["stop_reason"]
     assert [format_hex(h) for h in rep.residual_history] == case["history"]
     assert [format_hex(x) for x in rep.solution.data] == case["solution"]
+
+
+@pytest.mark.parametrize("prec", [53, 106, 424, 512, 640])
+def test_fixed_width_long_arithmetic_matches_generic(prec):
+    # the refinement loop's fixed-width add/sub/mul (fastfloat.h) against
+    # the generic big-integer path (bigfloat.py single-rounding semantics)
+    import ctypes
+    from paper_2107_12550_b200 import _native as nat
+    m = ctypes.c_int64()
+    assert nat.lib().mpcore_debug_longfloat_selftest(
+        40000, 1234 + prec, prec, ctypes.byref(m)) == 0
+    assert m.value == 0
