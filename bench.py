@@ -499,6 +499,96 @@ def run_dist(args):
     dist.destroy_process_group()
 
 
+def run_config1(args):
+    """BASELINE config 1: DD/TD/QD dense GEMM C = A*B, n = 2048 (the
+    reference's mat_mul_blocked, linalg.py:577-617; every output's chain
+    ascending in p from exact +0).  value = 2 n^3 / t; replicas for N > 1."""
+    world, rank, local, pg = dist_setup(args)
+    os.environ.setdefault("MPCORE_DEVICE", str(local))
+    from paper_2107_12550_b200 import _native as nat
+    from paper_2107_12550_b200.linalg import DeviceMatrix
+    L = nat.lib()
+    k, n = args.k, args.n
+    seed = 210712550 + 1
+    A = DeviceMatrix(k, n, n)
+    A.generate(0, n, seed)
+    B = DeviceMatrix(k, n, n)
+    B.generate(1, n, seed)
+    C = DeviceMatrix(k, n, n)
+
+    def step():
+        nat.check(L.mpcore_mat_mul(A.handle, B.handle, C.handle), "mat_mul")
+
+    for _ in range(args.warmup):
+        step()
+    nat.sync()
+    peak_add, peak_fma = nat.fp64_peak() if rank == 0 else (0.0, 0.0)
+    barrier(pg)
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+        nat.sync()
+        wall = time.perf_counter() - t0
+    ms = max_over_ranks(pg, wall * 1e3 / args.steps)
+    nat.prof_reset()
+    nat.prof_enable(True)
+    step()
+    nat.sync()
+    nat.prof_enable(False)
+    prof = nat.prof_read()
+    # e2e: host A, B (pinned) -> product -> host C
+    hA, hB, hC = (nat.PinnedBuffer((k, n, n)) for _ in range(3))
+    A.download(hA.array)
+    B.download(hB.array)
+    E1, E2, E3 = (DeviceMatrix(k, n, n) for _ in range(3))
+
+    def e2e_step():
+        nat.set_planes(E1.handle, hA.array)
+        nat.set_planes(E2.handle, hB.array)
+        nat.check(L.mpcore_mat_mul(E1.handle, E2.handle, E3.handle), "mm")
+        E3.download(hC.array)
+
+    e2e_step()
+    t0 = time.perf_counter()
+    for _ in range(max(1, min(args.steps, 3))):
+        e2e_step()
+    e2e_ms = max_over_ranks(pg, (time.perf_counter() - t0) * 1e3
+                            / max(1, min(args.steps, 3)))
+    assert hC.array.tobytes() == C.download().tobytes()
+    if rank != 0:
+        return
+    flops = 2.0 * n ** 3
+    instr = n ** 3 * MADD_INSTR[k]
+    gemm_ms = prof["gemm"][0] / max(1, prof["gemm"][1])
+    line = {
+        "metric": "%s GEMM eff. GFLOP/s (2n^3/s)" % NAMES[k],
+        "value": world * flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64x%d (%s, bit-exact EFT arithmetic)" % (k, NAMES[k]),
+        "data": "synthetic (seeded splitmix64 recipe, SURVEY 8d; seed %d)"
+                % seed,
+        "config": {"workload": "config1: %s GEMM n=%d" % (NAMES[k], n),
+                   "n": n, "k": k, "parallelism": "replicas x%d" % world,
+                   "l2": "A, B, C = 3 x %d MB (> L2)" % (k * n * n * 8 >> 20)},
+        "e2e": {"value": world * flops / (e2e_ms * 1e-3) / 1e9,
+                "unit": "GFLOP/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": 2 * k * n * n * 8,
+                "d2h_bytes_per_step": k * n * n * 8,
+                "path": "C ABI: set_planes(A, B) + mat_mul + get_planes(C)"},
+        "roofline": {"bound": "fp64", "kernel": "gemm_kernel",
+                     "achieved": instr / (gemm_ms * 1e-3) / 1e12,
+                     "peak": peak_add / 1e12, "unit": "T FP64 instr/s",
+                     "frac": instr / (gemm_ms * 1e-3) / peak_add
+                     if peak_add else None, "traffic": None},
+        "gpu_launches": int(sum(v[1] for v in prof.values())),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+
+
 def run_config3(args):
     """BASELINE config 3: TD-mpmath mixed-precision IR, n = 1024, A =
     U diag(sigma) W with kappa = 1e30 at 512 bits, rtol 1e-100, atol 0,
@@ -591,7 +681,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4])
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--dim", dest="n", type=int, default=None)
     ap.add_argument("--nb", type=int, default=0)
@@ -606,6 +696,9 @@ def main():
     elif args.config == 3:
         args.k = 3
         args.n = args.n or 1024
+    elif args.config == 1:
+        args.k = args.k or 2
+        args.n = args.n or 2048
     else:
         args.k = args.k or 3
         args.n = args.n or 2048
@@ -615,6 +708,8 @@ def main():
         run_dist(args)
     elif args.config == 3:
         run_config3(args)
+    elif args.config == 1:
+        run_config1(args)
     else:
         run_ours(args)
 
