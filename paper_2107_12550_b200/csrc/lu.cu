@@ -7,11 +7,14 @@
 //      rows, singular check (433-436), recip = div(1, pivot) (439),
 //      multipliers m_i = mul(A_ij, recip) (441) and the rank-1 update of the
 //      remaining panel columns A_ic = add(A_ic, mul(-m_i, A_jc)) (444-448).
-//   2. laswp_kernel: the same row exchanges, composed, on every column
-//      outside the panel (the reference swaps full rows, 430-431).
-//   3. trsm_kernel: U12 rows J..J+w-1 of the trailing columns, continuing
+//   2. swap_trsm_kernel: the same row exchanges, composed, on every column
+//      outside the panel (the reference swaps full rows, 430-431), and in
+//      the same pass U12 rows J..J+w-1 of the trailing columns, continuing
 //      each element's chain with the panel steps it had not seen yet.
-//   4. lu_update (gemm.cu): A22 <- fold_j add(A22, mul(-L21_ij, U12_jc)).
+//   3. lu_update (gemm.cu): A22 <- fold_j add(A22, mul(-L21_ij, U12_jc)).
+// (laswp_kernel and trsm_kernel are the stand-alone pieces behind the
+// distributed driver's mpcore_dev_laswp / mpcore_dev_trsm.)  Columns past
+// the m pivoted ones (right-hand sides) take every exchange and update.
 // Every element sees the same sequence of add(., mul(-m, u)) operations, in
 // the same order, as in the reference; blocking only changes when each link
 // runs (SURVEY finding 2).
