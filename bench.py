@@ -126,6 +126,21 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.samples)}
 
 
+class stdout_to_stderr:
+    """Route file descriptor 1 to 2 for a block (native libraries' prints)."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *a):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -399,8 +414,12 @@ def run_dist(args):
     if not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
-        dist.init_process_group("nccl", rank=rank, world_size=world,
-                                device_id=torch.device("cuda", local))
+        # NCCL announces itself on stdout at its first communicator: keep
+        # stdout for the one JSON line
+        with stdout_to_stderr():
+            dist.init_process_group("nccl", rank=rank, world_size=world,
+                                    device_id=torch.device("cuda", local))
+            dist.barrier()
     from paper_2107_12550_b200 import _native as nat
     from paper_2107_12550_b200.dist import (DeviceBackend, Layout, TorchComm,
                                             dist_lu_factor)
