@@ -358,11 +358,6 @@ cudaError_t panel_k(int n, MatView A, int J, int w, int32_t *d_swaps,
   int G = min(ws.G, max(1, (m + rows_target - 1) / rows_target));
   const int R = (m + G - 1) / G;
   size_t smem = panel_smem<K, W>(R);
-  static const size_t smem_min = [] {
-    const char *e = std::getenv("MPCORE_PANEL_SMEM_MIN");
-    return e ? (size_t)std::atol(e) : (size_t)0;
-  }();
-  if (smem < smem_min) smem = smem_min;
   // the poll keeps every slot's words in registers: size it to G so the
   // panel leaves room for update CTAs on its SMs (look-ahead overlap)
   if (G <= 64)
