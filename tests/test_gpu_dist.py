@@ -83,3 +83,31 @@ def test_tall_block_lu_matches_oracle(k, m, w):
     sw = be.lu_block(M, 0, 0, w)
     assert sw.tobytes() == sw_ref.tobytes()
     assert M.cpu().numpy().tobytes() == ref.tobytes()
+
+
+def test_config4_rank_invariance_large():
+    # SURVEY 8(c) config-4 plan: the column-block-cyclic factorisation is
+    # byte-identical for every rank count (here G = 1, 4, 8 virtual ranks
+    # on one GPU) at a size the oracle cannot reach; n = 16384 DD, nb = 256
+    k, n, nb, seed = 2, 16384, 256, 210712554
+    full = {}
+    for G in (1, 4, 8):
+        layout = Layout(n, nb, G)
+        be = DeviceBackend(k)
+        local = {}
+        for r in range(G):
+            M = be.alloc(n, layout.local_cols(r))
+            be.generate(M, layout, r, 0, seed)
+            local[r] = M
+        swaps = dist_lu_factor(be, LocalComm(), layout, local)
+        A = torch.empty((k, n, n), dtype=torch.float64, device="cuda")
+        for r, M in local.items():
+            A[:, :, torch.as_tensor(layout.global_columns(r),
+                                    device="cuda")] = M
+        del local
+        full[G] = (swaps, A)
+        if G != 1:
+            assert swaps.tobytes() == full[1][0].tobytes()
+            assert torch.equal(A.view(torch.int64), full[1][1].view(torch.int64))
+            del full[G]
+        torch.cuda.empty_cache()
