@@ -408,12 +408,29 @@ cudaError_t lu_swap_trsm(int k, MatView A, int J, int w, int c0, int c1,
   // CTAs of 4 warps: 4 columns (DD, a lane per row) or 8 (TD/QD)
   const int nl = (max(0, c1 - c0) + 3) / 4, nr = (max(0, c3 - c2) + 3) / 4;
   const int nl2 = (max(0, c1 - c0) + 7) / 8, nr2 = (max(0, c3 - c2) + 7) / 8;
+  static const int lpc16_cols = [] {
+    const char *e = std::getenv("MPCORE_TRSM_PAIR_COLS");
+    return e ? std::atoi(e) : 1200;
+  }();
   if (nl + nr == 0) return cudaSuccess;
   prof_begin(PROF_TRSM, s);
   switch (k) {
     case 2: swap_trsm_kernel<2, 32><<<nl + nr, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status); break;
-    case 3: swap_trsm_kernel<3, 16><<<nl2 + nr2, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status); break;
-    case 4: swap_trsm_kernel<4, 16><<<nl2 + nr2, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status); break;
+    // TD/QD: two columns per warp (fewer madd steps) while the columns
+    // fill the GPU; a lane per row (31 instead of 46 dependent steps) once
+    // the trailing block is small and the solve is latency-bound
+    case 3:
+      if (c3 - c2 >= lpc16_cols)
+        swap_trsm_kernel<3, 16><<<nl2 + nr2, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status);
+      else
+        swap_trsm_kernel<3, 32><<<nl + nr, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status);
+      break;
+    case 4:
+      if (c3 - c2 >= lpc16_cols)
+        swap_trsm_kernel<4, 16><<<nl2 + nr2, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status);
+      else
+        swap_trsm_kernel<4, 32><<<nl + nr, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status);
+      break;
     default: return cudaErrorInvalidValue;
   }
   prof_end(PROF_TRSM, s);
