@@ -210,6 +210,14 @@ template <int K> static void divk(const double *a, const double *b, double *o) {
 // Element (i, j) of plane c: p[c * plane + i * ld + j].
 
 // _lu_lanes (linalg.py:422-449).  Returns 0, or 3 with *sing = step.
+// np.argmax over |head| (linalg.py:429): the first NaN if any, else the
+// first maximum -- "m beats the best so far" in that order
+static inline bool pivot_better(double m, double best) {
+  if (std::isnan(best)) return false;
+  if (std::isnan(m)) return true;
+  return m > best;
+}
+
 template <int K>
 static int lu(int n, double *d, int32_t *swaps, int32_t *sing) {
   const size_t plane = (size_t)n * n;
@@ -220,7 +228,7 @@ static int lu(int n, double *d, int32_t *swaps, int32_t *sing) {
     double best = std::fabs(d[(size_t)j * n + j]);
     for (int i = j + 1; i < n; ++i) {
       double m = std::fabs(d[(size_t)i * n + j]);
-      if (m > best) { best = m; r = i; }
+      if (pivot_better(m, best)) { best = m; r = i; }
     }
     if (r != j) {  // full-row swap (linalg.py:430-431)
       for (int c = 0; c < K; ++c) {
@@ -280,7 +288,7 @@ static int lu_block(int m, int w, double *d, int64_t ld, int64_t pl,
     double best = std::fabs(d[(int64_t)j * ld + j]);
     for (int i = j + 1; i < m; ++i) {
       double v = std::fabs(d[(int64_t)i * ld + j]);
-      if (v > best) { best = v; r = i; }
+      if (pivot_better(v, best)) { best = v; r = i; }
     }
     if (r != j)
       for (int c = 0; c < K; ++c)

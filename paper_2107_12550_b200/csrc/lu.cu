@@ -69,10 +69,19 @@ __device__ __forceinline__ u64 ll_word(unsigned payload, unsigned seq) {
   return ((u64)payload << 32) | seq;
 }
 
-// (mag, row): larger magnitude wins; ties go to the smaller row
-// (np.argmax returns the first maximum, linalg.py:429).
+// Pivot order of np.argmax(|head|) (linalg.py:429): the first NaN if any,
+// else the first maximum.  Magnitudes are >= 0, so their bit patterns order
+// like the values, and a canonical NaN sorts above +inf.
+__device__ __forceinline__ unsigned long long mag_key(double m) {
+  return m != m ? 0x7FF8000000000000ull : (unsigned long long)__double_as_longlong(m);
+}
+// (mag, row): larger key wins, ties go to the smaller row; row INT_MAX is
+// "no candidate"
 __device__ __forceinline__ bool better(double m1, int r1, double m2, int r2) {
-  return m1 > m2 || (m1 == m2 && r1 < r2);
+  if (r2 == INT_MAX) return r1 != INT_MAX;
+  if (r1 == INT_MAX) return false;
+  const unsigned long long k1 = mag_key(m1), k2 = mag_key(m2);
+  return k1 > k2 || (k1 == k2 && r1 < r2);
 }
 
 #include "panel.cuh"

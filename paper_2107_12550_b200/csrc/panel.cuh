@@ -36,13 +36,13 @@ __device__ __forceinline__ void nb_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-// warp-wide first max of (mag >= 0 or -1, row): larger |head| first, then
-// the smaller row (np.argmax).  Non-negative doubles order like their bit
-// patterns, so three integer reductions decide it exactly.
+// warp-wide first max of (mag, row) in the order of better(): larger
+// mag_key first (NaN above everything), then the smaller row (np.argmax);
+// three integer reductions decide it exactly.
 __device__ __forceinline__ void warp_argmax(double mag, int row, double &out_mag,
                                             int &out_row) {
-  const bool valid = row != INT_MAX && mag >= 0.0;
-  unsigned long long b = valid ? (unsigned long long)__double_as_longlong(mag) : 0ull;
+  const bool valid = row != INT_MAX;
+  unsigned long long b = valid ? mag_key(mag) : 0ull;
   unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
   unsigned vmask = __ballot_sync(0xffffffffu, valid);
   if (!valid) hi = 0u;
