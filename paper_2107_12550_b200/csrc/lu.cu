@@ -71,17 +71,10 @@ __device__ __forceinline__ u64 ll_word(unsigned payload, unsigned seq) {
 
 // Pivot order of np.argmax(|head|) (linalg.py:429): the first NaN if any,
 // else the first maximum.  Magnitudes are >= 0, so their bit patterns order
-// like the values, and a canonical NaN sorts above +inf.
+// like the values; every NaN maps to one key above +inf.
 __device__ __forceinline__ unsigned long long mag_key(double m) {
-  return m != m ? 0x7FF8000000000000ull : (unsigned long long)__double_as_longlong(m);
-}
-// (mag, row): larger key wins, ties go to the smaller row; row INT_MAX is
-// "no candidate"
-__device__ __forceinline__ bool better(double m1, int r1, double m2, int r2) {
-  if (r2 == INT_MAX) return r1 != INT_MAX;
-  if (r1 == INT_MAX) return false;
-  const unsigned long long k1 = mag_key(m1), k2 = mag_key(m2);
-  return k1 > k2 || (k1 == k2 && r1 < r2);
+  const unsigned long long b = (unsigned long long)__double_as_longlong(m);
+  return b > 0x7FF0000000000000ull ? 0x7FF8000000000000ull : b;
 }
 
 #include "panel.cuh"

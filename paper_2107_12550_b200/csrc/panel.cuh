@@ -36,13 +36,13 @@ __device__ __forceinline__ void nb_arrive(int id, int count) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-// warp-wide first max of (mag, row) in the order of better(): larger
-// mag_key first (NaN above everything), then the smaller row (np.argmax);
-// three integer reductions decide it exactly.
-__device__ __forceinline__ void warp_argmax(double mag, int row, double &out_mag,
+// warp-wide first max of (key, row): larger mag_key first (NaN above
+// everything), then the smaller row (np.argmax); row INT_MAX = no candidate.
+// Three integer reductions decide it exactly.
+__device__ __forceinline__ void warp_argmax(unsigned long long key, int row,
                                             int &out_row) {
   const bool valid = row != INT_MAX;
-  unsigned long long b = valid ? mag_key(mag) : 0ull;
+  const unsigned long long b = valid ? key : 0ull;
   unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
   unsigned vmask = __ballot_sync(0xffffffffu, valid);
   if (!valid) hi = 0u;
@@ -51,13 +51,7 @@ __device__ __forceinline__ void warp_argmax(double mag, int row, double &out_mag
   unsigned mlo = __reduce_max_sync(0xffffffffu, lo_c);
   unsigned rc = (valid && hi == mhi && lo == mlo) ? (unsigned)row : 0xffffffffu;
   unsigned mrow = __reduce_min_sync(0xffffffffu, rc);
-  if (vmask == 0u) {
-    out_mag = -1.0;
-    out_row = INT_MAX;
-  } else {
-    out_row = (int)mrow;
-    out_mag = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
-  }
+  out_row = vmask == 0u ? INT_MAX : (int)mrow;
 }
 
 struct PanelSmem {
@@ -110,10 +104,10 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
   __syncthreads();
 
   // W0: local first max of column jj (rows >= J+jj) and its candidate words
-  auto w0_publish_max = [&](int jj, unsigned seq, double mag, int row) {
-    double bm;
+  auto w0_publish_max = [&](int jj, unsigned seq, unsigned long long key,
+                            int row) {
     int br;
-    warp_argmax(mag, row, bm, br);
+    warp_argmax(key, row, br);
     u64 *wd = ws.cand_words + ((int64_t)(jj & 1) * G + g) * LU_CAND_WORDS;
     if (lane == 0) {
       S.cand_row = br;
@@ -124,18 +118,20 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       st_volatile(wd + lane, ll_word((lane & 1) ? lo32(v) : hi32(v), seq));
     }
   };
+  // (each lane scans its rows in increasing order, so "strictly larger"
+  // keeps the first maximum; warp_argmax breaks ties across lanes by row)
   auto w0_publish_candidate = [&](int jj, unsigned seq) {
     const int j = J + jj;
-    double mag = -1.0;
+    unsigned long long key = 0ull;
     int row = INT_MAX;
     for (int r = lane; r < nr; r += 32) {
       int gi = rbeg + r;
       if (gi >= j) {
-        double v = fabs(at(r, jj)[0]);
-        if (better(v, gi, mag, row)) { mag = v; row = gi; }
+        const unsigned long long kv = mag_key(fabs(at(r, jj)[0]));
+        if (row == INT_MAX || kv > key) { key = kv; row = gi; }
       }
     }
-    w0_publish_max(jj, seq, mag, row);
+    w0_publish_max(jj, seq, key, row);
   };
   // H: publish the candidate row of column jj (+ row J+jj if owned)
   auto h_publish_rows = [&](int jj, unsigned seq, int row) {
@@ -229,7 +225,9 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
         if (__all_sync(0xffffffffu, done == (1u << SPL) - 1u)) break;
         __nanosleep(ws.poll_ns);
       }
-      double bm = -1.0;
+      // (a lane's slots hold increasing row ranges: "strictly larger"
+      // keeps the first maximum)
+      unsigned long long bk = 0ull;
       int br = INT_MAX;
       unsigned bw[2 * K];
 #pragma unroll
@@ -238,19 +236,18 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       for (int q = 0; q < SPL; ++q) {
         if (lane + 32 * q < G) {
           const int rr = (int)(wv[q][0] >> 32);
-          const double mm = fabs(__longlong_as_double(
-              (long long)((wv[q][2] & 0xffffffff00000000ull) | (wv[q][1] >> 32))));
-          if (rr != INT_MAX && better(mm, rr, bm, br)) {
-            bm = mm;
+          const unsigned long long kk = mag_key(fabs(__longlong_as_double(
+              (long long)((wv[q][2] & 0xffffffff00000000ull) | (wv[q][1] >> 32)))));
+          if (rr != INT_MAX && (br == INT_MAX || kk > bk)) {
+            bk = kk;
             br = rr;
 #pragma unroll
             for (int x = 0; x < 2 * K; ++x) bw[x] = (unsigned)(wv[q][1 + x] >> 32);
           }
         }
       }
-      double gm;
       int r;
-      warp_argmax(bm, br, gm, r);
+      warp_argmax(bk, br, r);
       trace(jj, 1);
       const int gw = (r - J) / R;
       if (g == 0 && lane == 0) swaps[j] = r;
@@ -291,7 +288,7 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       // one pass over the rows i > j: multiplier m_i = mul(A_ij, recip),
       // look-ahead update of column jj+1 and its local first max
       const bool ahead = jj + 1 < w;
-      double mag = -1.0;
+      unsigned long long mkey = 0ull;
       int mrow = INT_MAX;
       for (int rr = lane; rr < nr; rr += 32) {
         const int gi = rbeg + rr;
@@ -313,8 +310,8 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
             mc::madd<K>(acc, negm, u);
 #pragma unroll
             for (int c = 0; c < K; ++c) at(rr, jj + 1)[c] = acc[c];
-            const double v = fabs(acc[0]);
-            if (better(v, gi, mag, mrow)) { mag = v; mrow = gi; }
+            const unsigned long long kv = mag_key(fabs(acc[0]));
+            if (mrow == INT_MAX || kv > mkey) { mkey = kv; mrow = gi; }
           }
         }
       }
@@ -322,7 +319,7 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       trace(jj, 5);
       if (ahead) {
         __syncwarp();
-        w0_publish_max(jj + 1, seq + 1, mag, mrow);
+        w0_publish_max(jj + 1, seq + 1, mkey, mrow);
         trace(jj, 6);
       }
       __syncwarp();
