@@ -178,14 +178,75 @@ template <int K> MCI void mul_scalar(const double *a, double x, double *o) {
   for (int c = 0; c < K; ++c) two_prod(a[c], x, t[c], t[K + c]);
   cascade_compress<2 * K, K>(t, o);
 }
+// RN(1/b) when b lies well inside the normal range (|exponent| <= 423), else
+// 0: the hint that lets ddiv_y skip the division routine.
+MCI double recip_hint(double b) {
+  const unsigned eb = ((unsigned)__double2hiint(b) >> 20) & 0x7ffu;
+  return eb - 600u <= 846u ? __ddiv_rn(1.0, b) : 0.0;
+}
+// RN(a / b) given y = recip_hint(b), bit-identical to __ddiv_rn(a, b).
+// With y = RN(1/b): q0 = RN(a y) is within 1.5 ulp of a/b, one correction
+// q1 = RN(q0 + RN(a - q0 b) y) is within 1/2 ulp plus ~2^-51 ulp, and from
+// there r = a - q1 b is exact and RN(q1 + r y) = RN(a/b) (Markstein's
+// theorem: a/b is at least 2^-53 ulp / b from any midpoint, the error term
+// (a/b - q1)(by - 1) stays below it for b in [1, 2)).  Both operands within
+// 2^+-423 keep every intermediate normal; anything else (zero remainders,
+// huge/tiny values, Inf, NaN) takes __ddiv_rn.  tests/test_gpu_div.py and
+// tools/divcheck.cu check it against __ddiv_rn on hard cases.
+// (out of line: inlined, the compiler if-converts the routine's own fast
+// path into the caller and the select waits for it)
+static __device__ __noinline__ double ddiv_slow(double a, double b) {
+  return __ddiv_rn(a, b);
+}
+MCI double ddiv_y(double a, double b, double y) {
+  // the corrections run unconditionally; the range test overlaps them and
+  // only a rejected operand pays for the division routine
+  double q = __dmul_rn(a, y);
+  double r = __fma_rn(-q, b, a);
+  q = __fma_rn(r, y, q);
+  r = __fma_rn(-q, b, a);
+  q = __fma_rn(r, y, q);
+  const unsigned ea = ((unsigned)__double2hiint(a) >> 20) & 0x7ffu;
+  if (y == 0.0 || ea - 600u > 846u) q = ddiv_slow(a, b);
+  return q;
+}
 // _div_t: K+1 head-quotient digits of long division; b[0] != 0 required.
-template <int K> MCI void div(const double *a, const double *b, double *o) {
+// y = recip_hint(b[0]) (one division per divisor, off the digit chain).
+template <int K>
+MCI void div_y(const double *a, const double *b, double y, double *o) {
   double digits[K + 1], r[K];
 #pragma unroll
   for (int c = 0; c < K; ++c) r[c] = a[c];
 #pragma unroll
   for (int i = 0; i < K + 1; ++i) {
-    double qi = __ddiv_rn(r[0], b[0]);
+    double qi = ddiv_y(r[0], b[0], y);
+    digits[i] = qi;
+    if (i < K) {
+      double t[K], nr[K];
+      mul_scalar<K>(b, qi, t);
+#pragma unroll
+      for (int c = 0; c < K; ++c) t[c] = -t[c];
+      add<K>(r, t, nr);
+#pragma unroll
+      for (int c = 0; c < K; ++c) r[c] = nr[c];
+    }
+  }
+  cascade_compress<K + 1, K>(digits, o);
+}
+template <int K> MCI void div(const double *a, const double *b, double *o) {
+  div_y<K>(a, b, recip_hint(b[0]), o);
+}
+// div(1, b): the first digit RN(1/b[0]) is the hint itself
+template <int K> MCI void recip(const double *b, double *o) {
+  double digits[K + 1], r[K];
+  const double y = recip_hint(b[0]);
+  r[0] = 1.0;
+#pragma unroll
+  for (int c = 1; c < K; ++c) r[c] = 0.0;
+#pragma unroll
+  for (int i = 0; i < K + 1; ++i) {
+    double qi = i == 0 ? (y != 0.0 ? y : __ddiv_rn(1.0, b[0]))
+                       : ddiv_y(r[0], b[0], y);
     digits[i] = qi;
     if (i < K) {
       double t[K], nr[K];

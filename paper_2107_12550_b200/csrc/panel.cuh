@@ -275,10 +275,8 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
       if (singular) return;
       if (last) break;
       // recip = div(1, pivot): every lane computes the same value
-      double one[K], rc[K];
-#pragma unroll
-      for (int c = 0; c < K; ++c) one[c] = c == 0 ? 1.0 : 0.0;
-      mc::div<K>(one, pv, rc);
+      double rc[K];
+      mc::recip<K>(pv, rc);
       trace(jj, 2);
       nb_sync(B_ROW, PANEL_THREADS);  // pivot row staged, swap applied
       trace(jj, 3);

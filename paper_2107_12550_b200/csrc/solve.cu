@@ -164,6 +164,9 @@ sweep_kernel(int n, MatView LU, double *__restrict__ x, u64 *__restrict__ W,
 #pragma unroll
           for (int k = 0; k < K; ++k)
             Ld[k * TILE + r * PS + lane] = LU.p[k * LU.plane + row + r0 + lane];
+          // the row's division hint RN(1/U_rr) in the tile's pad column
+          if (BACK && lane == r)
+            Ld[r * PS + SB] = mc::recip_hint(LU.p[row + r0 + lane]);
         }
       }
       nb_arrive(BAR_STAGED);
@@ -317,7 +320,7 @@ sweep_kernel(int n, MatView LU, double *__restrict__ x, u64 *__restrict__ W,
           double u[K], qv[K];
 #pragma unroll
           for (int k = 0; k < K; ++k) u[k] = Ld[k * TILE + lane * PS + lane];
-          mc::div<K>(acc, u, qv);
+          mc::div_y<K>(acc, u, Ld[lane * PS + SB], qv);
 #pragma unroll
           for (int k = 0; k < K; ++k) acc[k] = qv[k];
           publish_x<K>(W, N, i, acc, seq);

@@ -31,10 +31,18 @@ __global__ void lat(double *out, long long *cyc, double s) {
   long long t8 = clock64();
   for (int i = 0; i < 20; ++i) { mc::div<3>(acc, x, q); x[0] = acc[0]; x[1] = acc[1]; x[2] = acc[2]; acc[0] = q[0]; acc[1] = q[1]; acc[2] = q[2]; }
   long long t9 = clock64();
-  out[threadIdx.x] = acc2[0] + acc2[1] + q[2] + acc[0];
+  const double y3 = mc::recip_hint(x[0]);
+  for (int i = 0; i < 20; ++i) { mc::div_y<3>(acc, x, y3, q); acc[0] = q[0]; acc[1] = q[1]; acc[2] = q[2]; }
+  long long t10 = clock64();
+  for (int i = 0; i < 20; ++i) { mc::recip<2>(acc2, q2); acc2[0] = q2[0]; acc2[1] = q2[1]; }
+  long long t11 = clock64();
+  for (int i = 0; i < 100; ++i) d = mc::ddiv_y(d, 1.37, 0.72992700729927);
+  long long t12 = clock64();
+  out[threadIdx.x] = acc2[0] + acc2[1] + q[2] + acc[0] + d;
   if (threadIdx.x == 0) {
     cyc[0] = t1 - t0; cyc[1] = t2 - t1; cyc[2] = t3 - t2; cyc[3] = t4 - t3;
     cyc[4] = t5 - t4; cyc[5] = t6 - t5; cyc[6] = t7 - t6; cyc[7] = t8 - t7; cyc[8] = t9 - t8;
+    cyc[9] = t10 - t9; cyc[10] = t11 - t10; cyc[11] = t12 - t11;
   }
 }
 
@@ -53,5 +61,8 @@ int main() {
   printf("DD div            %.1f cyc\n", h[6] / 20.0);
   printf("DD div (var b)    %.1f cyc\n", h[7] / 20.0);
   printf("TD div (var b)    %.1f cyc\n", h[8] / 20.0);
+  printf("TD div_y (hinted) %.1f cyc\n", h[9] / 20.0);
+  printf("DD recip (var b)  %.1f cyc\n", h[10] / 20.0);
+  printf("ddiv_y dep        %.1f cyc\n", h[11] / 100.0);
   return 0;
 }
