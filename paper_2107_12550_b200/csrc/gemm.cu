@@ -58,9 +58,8 @@ gemm_kernel(int M, int N, int KK, MatView A, MatView B, MatView C,
   const int tx = tid % TX, ty = tid / TX;
   const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
 
-  auto load_tile = [&](int stage, int k0) {
+  auto load_a = [&](int stage, int k0) {
     double *As = smem + stage * Cfg::STAGE;
-    double *Bs = As + K * Cfg::A_ELEMS;
     for (int e = tid; e < Cfg::A_ELEMS; e += NT) {
       int r = e / BK, q = e % BK;
       int gi = i0 + r, gq = k0 + q;
@@ -70,6 +69,9 @@ gemm_kernel(int M, int N, int KK, MatView A, MatView B, MatView C,
       for (int c = 0; c < K; ++c)
         cp_async8(As + c * Cfg::A_ELEMS + e, A.p + c * A.plane + off, ok);
     }
+  };
+  auto load_b = [&](int stage, int k0) {
+    double *Bs = smem + stage * Cfg::STAGE + K * Cfg::A_ELEMS;
     for (int e = tid; e < Cfg::B_ELEMS; e += NT) {
       int q = e / BN, cc = e % BN;
       int gq = k0 + q, gj = j0 + cc;
@@ -79,8 +81,14 @@ gemm_kernel(int M, int N, int KK, MatView A, MatView B, MatView C,
       for (int c = 0; c < K; ++c)
         cp_async8(Bs + c * Cfg::B_ELEMS + e, B.p + c * B.plane + off, ok);
     }
+  };
+  auto load_tile = [&](int stage, int k0) {
+    load_a(stage, k0);
+    load_b(stage, k0);
     cp_async_commit();
   };
+  const int ntiles = (KK + BK - 1) / BK;
+  if (ntiles > 0) load_tile(0, 0);
 
   double acc[TM][TN][K];
 #pragma unroll
@@ -96,8 +104,6 @@ gemm_kernel(int M, int N, int KK, MatView A, MatView B, MatView C,
                            : C.p[c * C.plane + (int64_t)gi * C.ld + gj];
     }
 
-  const int ntiles = (KK + BK - 1) / BK;
-  if (ntiles > 0) load_tile(0, 0);
   for (int kt = 0; kt < ntiles; ++kt) {
     if (kt + 1 < ntiles) {
       load_tile((kt + 1) & 1, (kt + 1) * BK);
@@ -181,23 +187,28 @@ struct Launcher {
 };
 
 // Candidate tiles per precision: (index, BM, BN, BK, TM, TN, min CTAs/SM),
-// 256 threads each.
+// 256 threads each; 6 and 7 are the 128- and 64-thread tiles for launches
+// too small to give every SM a 256-thread tile.
 #define MPK_TILES_DD(X)                                                       \
   X(0, 64, 64, 16, 4, 4, 2) X(1, 32, 64, 16, 2, 4, 2)                         \
   X(2, 64, 32, 16, 4, 2, 2) X(3, 32, 32, 16, 2, 2, 2)                         \
-  X(4, 16, 32, 16, 1, 2, 2) X(5, 32, 32, 16, 2, 2, 3)
+  X(4, 16, 32, 16, 1, 2, 2) X(5, 32, 32, 16, 2, 2, 3)                         \
+  X(6, 8, 16, 16, 1, 1, 4) X(7, 8, 8, 16, 1, 1, 8)
 #define MPK_TILES_XD(X)                                                       \
   X(0, 32, 32, 16, 2, 2, 1) X(1, 32, 16, 16, 2, 1, 2)                         \
   X(2, 16, 32, 16, 1, 2, 2) X(3, 16, 16, 16, 1, 1, 2)                         \
-  X(4, 8, 32, 16, 1, 1, 2) X(5, 32, 32, 16, 2, 2, 2)
+  X(4, 8, 32, 16, 1, 1, 2) X(5, 32, 32, 16, 2, 2, 2)                          \
+  X(6, 8, 16, 16, 1, 1, 4) X(7, 8, 8, 16, 1, 1, 8)
 // Their FP64 issue efficiency at a many-wave update shape (M = N = 8192,
 // KK = 32; tools/tile_sweep.py on B200), which the wave-aware chooser
-// weighs against tile quantisation.
-constexpr double TILE_EFF[3][6] = {
-    {0.940, 0.924, 0.918, 0.902, 0.852, 0.910},   // DD
-    {0.987, 0.981, 0.981, 0.976, 0.965, 0.990},   // TD
-    {0.975, 0.984, 0.987, 0.984, 0.976, 0.998}};  // QD
-constexpr int NTILES = 6;
+// weighs against tile quantisation.  (6, 7: only used below one tile per
+// SM, where the SM count, not the efficiency, decides.)
+constexpr double TILE_EFF[3][8] = {
+    {0.940, 0.924, 0.918, 0.902, 0.852, 0.910, 0.8, 0.8},    // DD
+    {0.987, 0.981, 0.981, 0.976, 0.965, 0.990, 0.95, 0.95},  // TD
+    {0.975, 0.984, 0.987, 0.984, 0.976, 0.998, 0.95, 0.95}}; // QD
+constexpr int NTILES = 8;
+constexpr unsigned SMALL_TILES = 0xc0u;
 
 struct TileInfo {
   int bm, bn, slots;
@@ -249,13 +260,43 @@ int tile_override() {
 // product is ~ ceil(tiles / resident slots) * tile area / efficiency; pick
 // the candidate minimising it (the trailing update shrinks every panel, so
 // a fixed tile wastes up to a wave per launch).
+//
+// A launch with fewer tiles than SMs leaves SMs idle and the busy ones run
+// a whole tile each: then the 128/64-thread tiles (SMALL_TILES) compete on
+// the outputs of the busiest SM, ceil(tiles / SMs) * tile area.
 template <int K, bool NEG_A, bool ZERO>
 int choose_tile(int M, int N, unsigned mask = 0x3fu) {
   const int forced = tile_override();
   if (forced >= 0 && forced < NTILES) return forced;
   const int sms = num_sms();
+  static const bool small_ok = std::getenv("MPCORE_NO_SMALL_TILES") == nullptr;
   int best = 0;
   double best_cost = 1e300;
+  for (int i = 0; i < NTILES; ++i) {
+    if (!(mask >> i & 1u)) continue;
+    const TileInfo t = tile_info<K, NEG_A, ZERO>(i);
+    if (t.slots <= 0) continue;
+    const int64_t tiles =
+        (int64_t)((M + t.bm - 1) / t.bm) * ((N + t.bn - 1) / t.bn);
+    if (tiles < sms && small_ok) {
+      // under one tile per SM: the busiest SM's outputs decide
+      int sbest = i;
+      double scost = (double)t.bm * t.bn / t.eff;
+      for (int q = 0; q < NTILES; ++q) {
+        if (!(SMALL_TILES >> q & 1u)) continue;
+        const TileInfo u = tile_info<K, NEG_A, ZERO>(q);
+        if (u.slots <= 0) continue;
+        const int64_t ut =
+            (int64_t)((M + u.bm - 1) / u.bm) * ((N + u.bn - 1) / u.bn);
+        const double c = (double)((ut + sms - 1) / sms) * u.bm * u.bn / u.eff;
+        if (c < scost * 0.999) {
+          scost = c;
+          sbest = q;
+        }
+      }
+      return sbest;
+    }
+  }
   for (int i = 0; i < NTILES; ++i) {
     if (!(mask >> i & 1u)) continue;
     const TileInfo t = tile_info<K, NEG_A, ZERO>(i);
@@ -277,6 +318,8 @@ template <int K, bool NEG_A, bool ZERO>
 cudaError_t launch(int M, int N, int KK, MatView A, MatView B, MatView C,
                    const int32_t *status, cudaStream_t s,
                    unsigned mask = 0x3fu) {
+  // (mask selects among the 256-thread tiles; small ones are added below
+  // one tile per SM)
   return launch_idx<K, NEG_A, ZERO>(choose_tile<K, NEG_A, ZERO>(M, N, mask),
                                     M, N, KK, A, B, C, status, s);
 }

@@ -79,6 +79,13 @@ __device__ __forceinline__ unsigned long long mag_key(double m) {
 
 #include "panel.cuh"
 
+// diagnostics: globaltimer into a trace slot (around the traced panel)
+__global__ void stamp_kernel(unsigned long long *dst) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *dst = t;
+}
+
 __global__ void lu_begin_kernel(unsigned *epoch, int32_t *status) {
   epoch[0] += 1u;
   status[0] = -1;
@@ -201,14 +208,25 @@ swap_trsm_kernel(MatView A, int J, int w, int c0, int c1, int c2, int c3,
     src[tid] = swap_list[2 * LU_MAX_W + tid];
   }
   if (right) {
-    // L11 (strictly lower part, negated): 8 independent loads per thread
+    // L11 (strictly lower part, negated): every load issued before the
+    // first shared store, so the 8 x K loads per thread share one L2 trip
+    constexpr int NIT = (LU_MAX_W * LU_MAX_W) / 128;
+    double lv[NIT][K];
 #pragma unroll
-    for (int it = 0; it < (LU_MAX_W * LU_MAX_W) / 128; ++it) {
+    for (int it = 0; it < NIT; ++it) {
+      const int e = tid + 128 * it, r = e / LU_MAX_W, q = e % LU_MAX_W;
+      const bool ok = q < r && r < w;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        lv[it][k] = ok ? A.p[k * A.plane + (int64_t)(J + r) * A.ld + J + q]
+                       : 0.0;
+    }
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
       const int e = tid + 128 * it, r = e / LU_MAX_W, q = e % LU_MAX_W;
       if (q < r && r < w) {
 #pragma unroll
-        for (int k = 0; k < K; ++k)
-          Ls[k][r][q] = -A.p[k * A.plane + (int64_t)(J + r) * A.ld + J + q];
+        for (int k = 0; k < K; ++k) Ls[k][r][q] = -lv[it][k];
       }
     }
     if (tid < LU_MAX_W) rsrc[tid] = J + tid;
@@ -415,28 +433,31 @@ cudaError_t lu_swap_trsm(int k, MatView A, int J, int w, int c0, int c1,
     return e ? std::atoi(e) : 1200;
   }();
   if (nl + nr == 0) return cudaSuccess;
+  cudaError_t e = cudaSuccess;
   prof_begin(PROF_TRSM, s);
+  auto go = [&](void (*kern)(MatView, int, int, int, int, int, int,
+                             const int32_t *, const int32_t *),
+                int grid) {
+    kern<<<grid, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status);
+    return cudaGetLastError();
+  };
   switch (k) {
-    case 2: swap_trsm_kernel<2, 32><<<nl + nr, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status); break;
+    case 2: e = go(swap_trsm_kernel<2, 32>, nl + nr); break;
     // TD/QD: two columns per warp (fewer madd steps) while the columns
     // fill the GPU; a lane per row (31 instead of 46 dependent steps) once
     // the trailing block is small and the solve is latency-bound
     case 3:
-      if (c3 - c2 >= lpc16_cols)
-        swap_trsm_kernel<3, 16><<<nl2 + nr2, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status);
-      else
-        swap_trsm_kernel<3, 32><<<nl + nr, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status);
+      e = c3 - c2 >= lpc16_cols ? go(swap_trsm_kernel<3, 16>, nl2 + nr2)
+                                : go(swap_trsm_kernel<3, 32>, nl + nr);
       break;
     case 4:
-      if (c3 - c2 >= lpc16_cols)
-        swap_trsm_kernel<4, 16><<<nl2 + nr2, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status);
-      else
-        swap_trsm_kernel<4, 32><<<nl + nr, 128, 0, s>>>(A, J, w, c0, c1, c2, c3, swap_list, status);
+      e = c3 - c2 >= lpc16_cols ? go(swap_trsm_kernel<4, 16>, nl2 + nr2)
+                                : go(swap_trsm_kernel<4, 32>, nl + nr);
       break;
     default: return cudaErrorInvalidValue;
   }
   prof_end(PROF_TRSM, s);
-  return cudaGetLastError();
+  return e;
 }
 
 // LU of the m x ncols matrix A: ncols == m is the square factorisation;
@@ -488,10 +509,17 @@ cudaError_t enqueue_lu(int k, int m, int ncols, MatView A, int32_t *d_swaps,
     // side stream, while the rest of this panel's update (disjoint
     // columns) runs here: the narrow update overlaps the wide one instead
     // of preceding it.
-    // (measured: TD/QD gain from the overlap, DD -- panel-bound -- does
-    // better with the narrow update ahead of the wide one on the main stream)
+    // (measured: TD/QD gain from the overlap while the rest of the update is
+    // long; DD -- panel-bound -- and the TD/QD tail, where the narrow update
+    // is on the panel chain, do better with it ahead of the wide one on the
+    // main stream: MPCORE_NEXT_MAIN_COLS, tools/nextcols_sweep.sh)
     static const char *nm_env = std::getenv("MPCORE_NEXT_ON_MAIN");
-    const bool next_on_main = nm_env ? std::atoi(nm_env) != 0 : k == 2;
+    static const int nm_cols = [] {
+      const char *e = std::getenv("MPCORE_NEXT_MAIN_COLS");
+      return e ? std::atoi(e) : 700;
+    }();
+    const bool next_on_main =
+        nm_env ? std::atoi(nm_env) != 0 : (k == 2 || rest_c - w2 < nm_cols);
     cudaStream_t ns = next_on_main ? s : ws.side;
     if (next_on_main &&
         (e = lu_update(k, rest_r, w2, w, sub(A, J2, J), sub(A, J, J2),
@@ -570,6 +598,8 @@ cudaError_t lu_begin(LuWork &ws, cudaStream_t s) {
 cudaError_t lu_panel(int k, int n, MatView A, int J, int w, int32_t *d_swaps,
                      LuWork &ws, int slot, cudaStream_t s) {
   prof_begin(PROF_PANEL, s);
+  const bool mark = ws.trace != nullptr && ws.trace_J == J;
+  if (mark) stamp_kernel<<<1, 1, 0, s>>>(ws.trace + 32 * 8 + 4);
   cudaError_t e = cudaErrorInvalidValue;
   if (w <= 16) {
     switch (k) {
@@ -584,6 +614,7 @@ cudaError_t lu_panel(int k, int n, MatView A, int J, int w, int32_t *d_swaps,
       case 4: e = panel_k<4, 32>(n, A, J, w, d_swaps, ws, slot, s); break;
     }
   }
+  if (mark) stamp_kernel<<<1, 1, 0, s>>>(ws.trace + 32 * 8 + 5);
   prof_end(PROF_PANEL, s);
   return e;
 }

@@ -13,6 +13,7 @@ buf = np.zeros(G * 33 * 8, dtype=np.uint64)
 nat.check(nat.lib().mpcore_debug_panel_trace(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), buf.size), "trace")
 t = buf.reshape(G, 33, 8).astype(np.int64)
 ks = t[:, 32, :4].copy()
+mk = t[0, 32, 4:6].copy()   # stamp kernels just before / after the launch
 g_used = int((t[:, 0, 7] > 0).sum())
 t = t[:g_used]
 names = ["poll", "pivot+div", "B_ROW", "mult", "B_REM", "la+pub"]
@@ -29,3 +30,6 @@ ks = ks[:g_used]
 e0 = ks[:, 0].min()
 print("kernel stamps (ns from first CTA entry; median/max over CTAs): entry %d/%d  prologue-done %d/%d  loop-done %d/%d  exit %d/%d" % tuple(
     v for c in range(4) for v in (np.median(ks[:, c] - e0), (ks[:, c] - e0).max())))
+if mk[0] > 0:
+    print("stream stamps (ns): before-launch -> first CTA entry %d, last CTA exit -> after-launch %d" % (
+        e0 - mk[0], mk[1] - ks[:, 3].max()))
