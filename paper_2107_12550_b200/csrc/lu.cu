@@ -430,7 +430,7 @@ cudaError_t lu_swap_trsm(int k, MatView A, int J, int w, int c0, int c1,
   const int nl2 = (max(0, c1 - c0) + 7) / 8, nr2 = (max(0, c3 - c2) + 7) / 8;
   static const int lpc16_cols = [] {
     const char *e = std::getenv("MPCORE_TRSM_PAIR_COLS");
-    return e ? std::atoi(e) : 1200;
+    return e ? std::atoi(e) : 800;
   }();
   if (nl + nr == 0) return cudaSuccess;
   cudaError_t e = cudaSuccess;
