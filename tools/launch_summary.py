@@ -1,5 +1,5 @@
 """Summarise an ncu --csv launch list (gpu__time_duration.sum) per kernel.
-usage: launch_summary.py CSV"""
+usage: launch_summary.py CSV [--by-kernel]"""
 import csv, collections, sys
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = None
@@ -11,7 +11,8 @@ for r in rows:
     if hdr and len(r) == len(hdr):
         d = dict(zip(hdr, r))
         name = d['Kernel Name'].split('(')[0].replace('void ', '').replace('(anonymous namespace)::', '')
-        name = name + (' ' + d['Grid Size'] if 'gemm' in name else '')
+        if '--by-kernel' not in sys.argv:
+            name = name + (' ' + d['Grid Size'] if 'gemm' in name else '')
         agg.setdefault(name, []).append(float(d['Metric Value'].replace(',', '')) / 1e3)
 tot = sum(sum(v) for v in agg.values())
 for k, v in agg.items():
