@@ -590,10 +590,29 @@ int32_t mpcore_lu_solve(uint64_t lu_h, uint64_t piv_h, uint64_t b_h,
 }  // extern "C"
 
 namespace {
+// Device buffers of the IR's short side, kept across refinement calls
+// (grow-only): the same addresses every call, so the LU's captured launch
+// graph (keyed on the matrix pointer) is replayed instead of re-captured.
+// One refinement at a time uses it; a concurrent one allocates its own.
+struct IrWorkspace {
+  std::atomic<bool> busy{false};
+  double *a = nullptr, *b = nullptr, *x = nullptr;
+  int32_t *perm = nullptr;
+  size_t acap = 0, bcap = 0, xcap = 0, pcap = 0;
+};
+IrWorkspace &ir_ws() {
+  static IrWorkspace w;
+  return w;
+}
+
 // The IR's short side on the GPU: factors stay resident in HBM.
 class GpuShortSolver : public mpr::ShortSolver {
  public:
   ~GpuShortSolver() override {
+    if (shared_) {
+      ir_ws().busy.store(false);
+      return;
+    }
     if (a_ || perm_ || b_ || x_) {
       DevLock L;
       if (a_) cudaFree(a_);
@@ -602,23 +621,50 @@ class GpuShortSolver : public mpr::ShortSolver {
       if (x_) cudaFree(x_);
     }
   }
-  int factor(int k, int n, const std::vector<double> &a,
+  int factor(int k, int n, const double *a,
              std::string &err) override {
     k_ = k;
     n_ = n;
     DevLock L;
     if (L.st) { err = g_err; return L.st; }
     Device &D = device();
-    cudaError_t e;
+    cudaError_t e = cudaSuccess;
     size_t mb = (size_t)k * n * n * sizeof(double), vb = (size_t)k * n * 8;
-    if ((e = cudaMalloc(&a_, mb)) != cudaSuccess ||
-        (e = cudaMalloc(&b_, vb)) != cudaSuccess ||
-        (e = cudaMalloc(&x_, vb)) != cudaSuccess ||
-        (e = cudaMalloc(&perm_, (size_t)n * 4)) != cudaSuccess) {
+    bool expected = false;
+    if (!shared_ && a_ == nullptr &&
+        ir_ws().busy.compare_exchange_strong(expected, true))
+      shared_ = true;
+    if (shared_) {
+      IrWorkspace &w = ir_ws();
+      auto grow = [&](void **p, size_t &cap, size_t need) {
+        if (cap >= need) return cudaSuccess;
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+        cap = 0;
+        cudaError_t r = cudaMalloc(p, need);
+        if (r == cudaSuccess) cap = need;
+        return r;
+      };
+      if ((e = grow((void **)&w.a, w.acap, mb)) == cudaSuccess &&
+          (e = grow((void **)&w.b, w.bcap, vb)) == cudaSuccess &&
+          (e = grow((void **)&w.x, w.xcap, vb)) == cudaSuccess)
+        e = grow((void **)&w.perm, w.pcap, (size_t)n * 4);
+      if (e != cudaSuccess) {
+        err = cudaGetErrorString(e);
+        return MPCORE_INTERNAL;
+      }
+      a_ = w.a;
+      b_ = w.b;
+      x_ = w.x;
+      perm_ = w.perm;
+    } else if ((e = cudaMalloc(&a_, mb)) != cudaSuccess ||
+               (e = cudaMalloc(&b_, vb)) != cudaSuccess ||
+               (e = cudaMalloc(&x_, vb)) != cudaSuccess ||
+               (e = cudaMalloc(&perm_, (size_t)n * 4)) != cudaSuccess) {
       err = cudaGetErrorString(e);
       return MPCORE_INTERNAL;
     }
-    if ((e = cudaMemcpy(a_, a.data(), mb, cudaMemcpyHostToDevice)) !=
+    if ((e = cudaMemcpy(a_, a, mb, cudaMemcpyHostToDevice)) !=
         cudaSuccess) {
       err = cudaGetErrorString(e);
       return MPCORE_INTERNAL;
@@ -669,6 +715,7 @@ class GpuShortSolver : public mpr::ShortSolver {
 
  private:
   int k_ = 0, n_ = 0;
+  bool shared_ = false;  // buffers borrowed from ir_ws()
   double *a_ = nullptr, *b_ = nullptr, *x_ = nullptr;
   int32_t *perm_ = nullptr;
 };

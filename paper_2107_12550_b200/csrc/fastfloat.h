@@ -8,7 +8,9 @@
 // big-integer path (mpcore_debug_longfloat_selftest).
 #pragma once
 #include <cstdint>
+#include <cmath>
 #include <cstring>
+#include <x86intrin.h>
 
 #include "bignum.h"
 
@@ -161,6 +163,294 @@ inline F add(const F &a, const F &b, int p) {
     }
   }
   return round_to(sign, w, nw, y.exp, p);
+}
+
+// ---- compile-time-width kernels (N = ceil(p / 64) limbs) -----------------
+// Same results as add / mul above (the exact value rounded once to p bits,
+// half to even), computed the way a floating-point adder does it: the
+// smaller operand is shifted right into a frame with one 64-bit guard limb
+// and a sticky bit, instead of shifting the larger one left into a window
+// of p + d bits.  In the frame, bit i of x's mantissa sits at i + 64.
+
+// top set bit of a (W limbs), -1 if zero
+template <int W> inline int top_bit(const uint64_t *a) {
+  for (int i = W - 1; i >= 0; --i)
+    if (a[i]) return 64 * i + 63 - __builtin_clzll(a[i]);
+  return -1;
+}
+// out[0..N) = a[0..W) >> s (0 <= s < 64 W), rounded to nearest even using
+// the bits shifted out plus `sticky`; returns true when the increment
+// carried to bit p (the caller renormalises)
+template <int W, int N>
+inline bool shr_round(const uint64_t *a, int s, bool sticky, int p,
+                      uint64_t *out) {
+  // zero-padded copy: out limb i reads pad[i + q], pad[i + q + 1]
+  uint64_t pad[W + N + 2];
+#pragma GCC unroll 32
+  for (int i = 0; i < W; ++i) pad[i] = a[i];
+#pragma GCC unroll 32
+  for (int i = W; i < W + N + 2; ++i) pad[i] = 0;
+  const int q = s >> 6, r = s & 63;
+  const uint64_t *src = pad + q;
+  if (r) {
+#pragma GCC unroll 16
+    for (int i = 0; i < N; ++i)
+      out[i] = (src[i] >> r) | (src[i + 1] << (64 - r));
+  } else {
+#pragma GCC unroll 16
+    for (int i = 0; i < N; ++i) out[i] = src[i];
+  }
+  if (s == 0) return false;
+  const int rb = s - 1;  // round bit position
+  if (!((a[rb >> 6] >> (rb & 63)) & 1u)) return false;
+  bool below = sticky;
+  if (!below) {
+    const int full = rb >> 6, rem = rb & 63;
+    for (int l = 0; l < full && !below; ++l) below = a[l] != 0;
+    if (!below && rem) below = (a[full] & ((1ull << rem) - 1ull)) != 0;
+  }
+  if (!below && !(out[0] & 1u)) return false;
+  bool carry = true;
+  for (int i = 0; i < N && carry; ++i) carry = ++out[i] == 0;
+  // rounded up to 2^p?
+  const int pl = p >> 6, pb = p & 63;
+  return carry || (pl < N && ((out[pl] >> pb) & 1u));
+}
+inline void set_pow2(F &r, int p) {  // mantissa 2^(p-1)
+  for (int i = 0; i < NL; ++i) r.m[i] = 0;
+  r.m[(p - 1) >> 6] = 1ull << ((p - 1) & 63);
+}
+
+template <int N> inline F add_t(const F &a, const F &b, int p) {
+  if (a.sign == 0) return b;
+  if (b.sign == 0) return a;
+  const F &x = a.exp >= b.exp ? a : b;
+  const F &y = a.exp >= b.exp ? b : a;
+  const int64_t d64 = x.exp - y.exp;
+  // y below a quarter ulp of x never moves the rounded result
+  if (d64 >= p + 3) return x;
+  const int d = (int)d64;
+  constexpr int W = N + 2;
+  uint64_t X[W], Y[W], S[W];
+  X[0] = 0;
+#pragma GCC unroll 16
+  for (int i = 0; i < N; ++i) X[i + 1] = x.m[i];
+  X[N + 1] = 0;
+  // Y = (y.m << 64) >> d, sticky = the bits shifted out.  ys[j] = limb j
+  // of y.m << 64, zero-padded so ys[i + q + 1] is in range (q <= N + 1)
+  const int q = d >> 6, r = d & 63;
+  uint64_t ys[2 * W + 2];
+  ys[0] = 0;
+#pragma GCC unroll 16
+  for (int i = 0; i < N; ++i) ys[i + 1] = y.m[i];
+#pragma GCC unroll 32
+  for (int i = N + 1; i < 2 * W + 2; ++i) ys[i] = 0;
+  const uint64_t *src = ys + q;
+  if (r) {
+#pragma GCC unroll 16
+    for (int i = 0; i < W; ++i) Y[i] = (src[i] >> r) | (src[i + 1] << (64 - r));
+  } else {
+#pragma GCC unroll 16
+    for (int i = 0; i < W; ++i) Y[i] = src[i];
+  }
+  bool sticky = false;
+  for (int j = 1; j < q; ++j) sticky |= ys[j] != 0;
+  if (r) sticky |= (ys[q] & ((1ull << r) - 1ull)) != 0;
+  int sign = x.sign;
+  if (x.sign == y.sign) {
+    unsigned char cf = 0;
+#pragma GCC unroll 16
+    for (int i = 0; i < W; ++i)
+      cf = _addcarry_u64(cf, X[i], Y[i], (unsigned long long *)&S[i]);
+  } else {
+    const uint64_t *P = X, *M = Y;
+    if (d == 0) {  // equal exponents: order the mantissas
+      int c = 0;
+      for (int i = W - 1; i >= 0 && c == 0; --i)
+        if (X[i] != Y[i]) c = X[i] > Y[i] ? 1 : -1;
+      if (c == 0) return F();
+      if (c < 0) {
+        P = Y;
+        M = X;
+        sign = y.sign;
+      }
+    }
+    // P - M - sticky: a lost fraction of M borrows one unit (the remaining
+    // fraction is still nonzero, so sticky stays set)
+    unsigned char bf = sticky ? 1 : 0;
+#pragma GCC unroll 16
+    for (int i = 0; i < W; ++i)
+      bf = _subborrow_u64(bf, P[i], M[i], (unsigned long long *)&S[i]);
+  }
+  const int t = top_bit<W>(S);
+  F res;
+  if (t < 0) return res;
+  res.sign = sign;
+  for (int i = N; i < NL; ++i) res.m[i] = 0;
+  if (t < p) {
+    // fewer than p + 1 bits: exact (bits are lost only for d > 64, and
+    // then the result keeps at least p + 62 bits in the frame)
+    const int sh = p - 1 - t;
+    shl_into(S, W, sh, res.m, N);
+    res.exp = x.exp - 64 - sh;
+    return res;
+  }
+  const int sh = t - p + 1;
+  res.exp = x.exp - 64 + sh;
+  if (shr_round<W, N>(S, sh, sticky, p, res.m)) {
+    set_pow2(res, p);
+    res.exp += 1;
+  }
+  return res;
+}
+
+template <int N> inline F mul_t(const F &a, const F &b, int p) {
+  if (a.sign == 0 || b.sign == 0) return F();
+  // column-wise (Comba): the partial products of a column are independent
+  // and accumulate into a three-word sum
+  uint64_t w[2 * N];
+  unsigned long long c0 = 0, c1 = 0, c2 = 0;
+#pragma GCC unroll 16
+  for (int k = 0; k < 2 * N - 1; ++k) {
+#pragma GCC unroll 16
+    for (int i = 0; i < N; ++i) {
+      const int j = k - i;
+      if (j < 0 || j >= N) continue;
+      const unsigned __int128 pr = (unsigned __int128)a.m[i] * b.m[j];
+      unsigned char cf = _addcarry_u64(0, c0, (uint64_t)pr, &c0);
+      cf = _addcarry_u64(cf, c1, (uint64_t)(pr >> 64), &c1);
+      c2 += cf;
+    }
+    w[k] = c0;
+    c0 = c1;
+    c1 = c2;
+    c2 = 0;
+  }
+  w[2 * N - 1] = c0;
+  // the product of two p-bit mantissas has 2p or 2p - 1 bits
+  const int top = 2 * p - 1;
+  const bool full = (w[top >> 6] >> (top & 63)) & 1u;
+  const int sh = full ? p : p - 1;
+  F res;
+  res.sign = a.sign * b.sign;
+  for (int i = N; i < NL; ++i) res.m[i] = 0;
+  res.exp = a.exp + b.exp + sh;
+  if (shr_round<2 * N, N>(w, sh, false, p, res.m)) {
+    set_pow2(res, p);
+    res.exp += 1;
+  }
+  return res;
+}
+
+// bf_to_multicomp on a fixed-width value (bigfloat.py:419-432, as
+// bn::to_multicomp): k heads, each the nearest binary64 (half to even),
+// peeled off exactly.  Returns false, leaving `out` undefined, when a head
+// would fall outside the normal binary64 range (the caller then takes the
+// generic path, which reproduces ldexp's subnormal rounding and overflow).
+template <int N> inline bool to_multicomp_t(F r, int k, int p, double *out) {
+  for (int c = 0; c < k; ++c) {
+    if (r.sign == 0) {
+      out[c] = 0.0;
+      continue;
+    }
+    uint64_t h;
+    int64_t E;  // head = h * 2^E, h <= 2^53
+    const int sh = p > 53 ? p - 53 : 0;
+    if (sh == 0) {
+      h = r.m[0];
+      E = r.exp;
+    } else {
+      const int q = sh >> 6, rr = sh & 63;
+      const uint64_t lo = r.m[q], hi = q + 1 < N ? r.m[q + 1] : 0;
+      h = (rr ? (lo >> rr) | (hi << (64 - rr)) : lo) & ((1ull << 53) - 1ull);
+      const int rb = sh - 1;
+      const bool half = (r.m[rb >> 6] >> (rb & 63)) & 1u;
+      bool below = false;
+      for (int l = 0; l < (rb >> 6) && !below; ++l) below = r.m[l] != 0;
+      if (!below && (rb & 63))
+        below = (r.m[rb >> 6] & ((1ull << (rb & 63)) - 1ull)) != 0;
+      if (half && (below || (h & 1u))) ++h;  // may reach 2^53 (exact)
+      E = r.exp + sh;
+    }
+    const int top = 63 - __builtin_clzll(h);
+    if (E + top < -1022 || E + top > 1023) return false;
+    const double v = std::ldexp((double)h, (int)E);
+    out[c] = r.sign < 0 ? -v : v;
+    if (c + 1 == k) break;
+    // r - head, exact: (m - (h << sh)) * 2^exp
+    uint64_t hv[N + 1], mm[N + 1], d[N + 1];
+    for (int i = 0; i <= N; ++i) hv[i] = 0;
+    {
+      const int q = sh >> 6, rr = sh & 63;
+      hv[q] |= h << rr;
+      if (rr && q + 1 <= N) hv[q + 1] |= h >> (64 - rr);
+    }
+    for (int i = 0; i < N; ++i) mm[i] = r.m[i];
+    mm[N] = 0;
+    int cmp = 0;
+    for (int i = N; i >= 0 && cmp == 0; --i)
+      if (mm[i] != hv[i]) cmp = mm[i] > hv[i] ? 1 : -1;
+    if (cmp == 0) {
+      r = F();
+      continue;
+    }
+    const uint64_t *P = cmp > 0 ? mm : hv, *M = cmp > 0 ? hv : mm;
+    unsigned char bf = 0;
+    for (int i = 0; i <= N; ++i)
+      bf = _subborrow_u64(bf, P[i], M[i], (unsigned long long *)&d[i]);
+    const int t = top_bit<N + 1>(d);
+    F nr;
+    nr.sign = cmp > 0 ? r.sign : -r.sign;
+    for (int i = 0; i < NL; ++i) nr.m[i] = 0;
+    shl_into(d, N + 1, p - 1 - t, nr.m, N);
+    nr.exp = r.exp - (p - 1 - t);
+    r = nr;
+  }
+  return true;
+}
+
+// runtime dispatch on the limb count
+#define FF_DISPATCH(FN, ...)             \
+  switch ((p + 63) >> 6) {               \
+    case 1: return FN<1>(__VA_ARGS__);   \
+    case 2: return FN<2>(__VA_ARGS__);   \
+    case 3: return FN<3>(__VA_ARGS__);   \
+    case 4: return FN<4>(__VA_ARGS__);   \
+    case 5: return FN<5>(__VA_ARGS__);   \
+    case 6: return FN<6>(__VA_ARGS__);   \
+    case 7: return FN<7>(__VA_ARGS__);   \
+    case 8: return FN<8>(__VA_ARGS__);   \
+    case 9: return FN<9>(__VA_ARGS__);   \
+    default: return FN<10>(__VA_ARGS__); \
+  }
+inline F fadd(const F &a, const F &b, int p) { FF_DISPATCH(add_t, a, b, p) }
+inline F fmul(const F &a, const F &b, int p) { FF_DISPATCH(mul_t, a, b, p) }
+inline bool to_multicomp(const F &r, int k, int p, double *out) {
+  FF_DISPATCH(to_multicomp_t, r, k, p, out)
+}
+#undef FF_DISPATCH
+
+// a binary64 value exactly, as a p-bit fixed-width value (p >= 53)
+inline F from_double(double x, int p) {
+  F r;
+  if (x == 0.0) return r;
+  int e;
+  const double f = std::frexp(std::fabs(x), &e);  // f in [0.5, 1)
+  uint64_t m = (uint64_t)std::ldexp(f, 53);         // exact, 53 bits
+  r.sign = x < 0 ? -1 : 1;
+  const int tz = __builtin_ctzll(m);
+  m >>= tz;
+  const int len = 64 - __builtin_clzll(m);
+  const uint64_t w[1] = {m};
+  for (int i = 0; i < NL; ++i) r.m[i] = 0;
+  shl_into(w, 1, p - len, r.m, NL);
+  r.exp = (int64_t)e - 53 + tz - (p - len);
+  return r;
+}
+// a value held at precision q, rounded once to p <= q bits
+inline F round(const F &a, int q, int p) {
+  if (a.sign == 0 || q == p) return a;
+  return round_to(a.sign, a.m, NL, a.exp, p);
 }
 
 inline F neg(const F &a) {

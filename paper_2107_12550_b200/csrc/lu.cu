@@ -683,7 +683,13 @@ cudaError_t lu_factor(int k, int m, int ncols, MatView A, int32_t *d_swaps,
       e = cudaStreamEndCapture(s, &graph);
       if (ee != cudaSuccess) return ee;
       if (e != cudaSuccess) return e;
-      e = cudaGraphInstantiate(&exec, graph, 0);
+      // node priorities (the panel's high-priority launch attribute) are
+      // ignored by a graph unless asked for: without them the panel waits
+      // behind the trailing update's CTAs for SM slots
+      static const unsigned gflags =
+          std::getenv("MPCORE_GRAPH_NO_PRIO") ? 0u
+                                              : cudaGraphInstantiateFlagUseNodePriority;
+      e = cudaGraphInstantiate(&exec, graph, gflags);
       cudaGraphDestroy(graph);
       if (e != cudaSuccess) return e;
       if (gc.entries.size() >= 512) {  // tall blocks: one shape per panel

@@ -11,10 +11,15 @@
 #include "fastfloat.h"
 
 #include <algorithm>
+#include <atomic>
+#include <climits>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <fstream>
+#include <memory>
 #include <sstream>
 #include <thread>
 
@@ -281,10 +286,9 @@ static void par_rows(size_t n, int threads, F f) {
   for (auto &t : ts) t.join();
 }
 
-static int to_planes(const std::vector<BF> &v, int k, std::vector<double> &out,
+static int to_planes(const std::vector<BF> &v, int k, double *out,
                      size_t count, std::string &err, int threads = 1) {
-  out.assign((size_t)k * count, 0.0);
-  std::vector<char> bad(threads > 0 ? threads : 1, 0);
+  std::vector<char> bad(1, 0);
   par_rows(count, threads, [&](size_t a, size_t b) {
     double c[4];
     for (size_t e = a; e < b; ++e) {
@@ -302,6 +306,19 @@ static int to_planes(const std::vector<BF> &v, int k, std::vector<double> &out,
   return 0;
 }
 
+// uninitialised heap buffer (no zero fill: first touch by the filling
+// threads); alloc() -> false when out of memory
+template <class T> struct RawBuf {
+  T *p = nullptr;
+  bool alloc(size_t n) {
+    p = static_cast<T *>(std::malloc(n * sizeof(T) + 1));
+    return p != nullptr;
+  }
+  T &operator[](size_t i) { return p[i]; }
+  const T &operator[](size_t i) const { return p[i]; }
+  ~RawBuf() { std::free(p); }
+};
+
 static BF norm2(const std::vector<BF> &v, int64_t p) {
   BF acc;
   for (const BF &s : v) acc = lf_add(acc, lf_mul(s, s, p), p);
@@ -312,6 +329,17 @@ using Clock = std::chrono::steady_clock;
 static double secs(Clock::time_point a, Clock::time_point b) {
   return std::chrono::duration<double>(b - a).count();
 }
+
+// MPCORE_REFINE_TIMERS=1: per-phase host times on stderr (diagnostics)
+struct PhaseLog {
+  bool on = std::getenv("MPCORE_REFINE_TIMERS") != nullptr;
+  Clock::time_point t = Clock::now();
+  void mark(const char *what) {
+    const auto u = Clock::now();
+    if (on) std::fprintf(stderr, "[refine] %-22s %8.2f ms\n", what, secs(t, u) * 1e3);
+    t = u;
+  }
+};
 
 int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
                 int short_k, int long_bits, const char *rtol_s,
@@ -333,60 +361,92 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
   if (rtol.sign < 0 || atol.sign < 0) { err = "tolerances must be nonnegative"; return 6; }
   if (rtol.sign == 0 && atol.sign == 0) { err = "rtol and atol cannot both be zero"; return 6; }
   const auto t0 = Clock::now();
+  PhaseLog plog;
   // re-round into the working context (convert_* BfDomain -> BfDomain)
   par_rows(Avals.size(), threads, [&](size_t a, size_t b) {
     for (size_t e = a; e < b; ++e) Avals[e] = lf_round(Avals[e], p);
   });
   for (auto &v : Bvals) v = lf_round(v, p);
+  plog.mark("round A, b");
   // short copies; transfer precision max(long, 53k+64)+8 (linalg.py:743)
   const int64_t p_in = std::max<int64_t>(p, 53 * k + 64) + 8;
-  std::vector<double> a_pl, b_pl, x_pl;
-  if ((st = to_planes(Avals, k, a_pl, (size_t)n * n, err, threads))) return st;
-  if ((st = to_planes(Bvals, k, b_pl, (size_t)n, err))) return st;
-  const auto t1 = Clock::now();
-  if ((st = S.factor(k, n, a_pl, err))) return st;
-  const auto t2 = Clock::now();
-  double t_solve = 0, t_res = 0;
-  auto timed_solve = [&](const std::vector<double> &rhs) {
-    const auto a = Clock::now();
-    const int r = S.solve(rhs, x_pl, err);
-    t_solve += secs(a, Clock::now());
-    return r;
-  };
-  if ((st = timed_solve(b_pl))) return st;
-  auto lift = [&](const std::vector<double> &pl, std::vector<BF> &x) {
-    x.resize(n);
-    double c[4];
-    for (int i = 0; i < n; ++i) {
-      for (int q = 0; q < k; ++q) c[q] = pl[(size_t)q * n + i];
-      x[i] = lf_round(from_components(c, k, p_in), p);
-    }
-  };
-  std::vector<BF> x;
-  lift(x_pl, x);
-  // ||A||_F, row-major accumulation (linalg.py:692-700); the squares are
-  // independent: formed on all threads, then summed in the reference's order
-  const bool fast = p <= 64 * ff::NL;   // fixed-width path (fastfloat.h)
+  const bool fast = p_in <= 64 * ff::NL;   // fixed-width path (fastfloat.h)
   const int pi = (int)p;
-  std::vector<ff::F> Af, Bf;
-  if (fast) {
-    Af.resize(Avals.size());
-    par_rows(Avals.size(), threads, [&](size_t a, size_t b) {
-      for (size_t e = a; e < b; ++e) Af[e] = ff::from_bf(Avals[e], pi);
-    });
-    Bf.resize(n);
-    for (int i = 0; i < n; ++i) Bf[i] = ff::from_bf(Bvals[i], pi);
+  const size_t nn = (size_t)n * n;
+  // n x n buffers are first touched by the threads that fill them (a
+  // zero-filled std::vector would page them in on one thread)
+  RawBuf<double> a_pl;
+  RawBuf<ff::F> Af, Sq;
+  if (!a_pl.alloc((size_t)k * nn) ||
+      (fast && (!Af.alloc(nn) || !Sq.alloc(nn)))) {
+    err = "out of host memory";
+    return 6;
   }
+  std::vector<double> b_pl((size_t)k * n), x_pl;
+  // ||A||_F, row-major accumulation (linalg.py:692-700): the squares are
+  // formed by the conversion pass on all threads; their sum, sequential in
+  // the reference's order, runs on its own thread, following the pass
+  // (per-worker progress counters) and then overlapping the GPU factor and
+  // the first solve
   BF a_fro;
+  ff::F fro_acc;
+  // (declared before the thread: they outlive its join)
+  const int T = (int)std::max<size_t>(1, std::min<size_t>((size_t)threads, nn));
+  std::unique_ptr<std::atomic<size_t>[]> done(new std::atomic<size_t>[T]);
+  std::atomic<bool> abort_sum{false};
+  for (int t = 0; t < T; ++t) done[t].store(0);
+  std::thread fro;
+  struct Joiner {  // every return below joins the summing thread
+    std::thread &t;
+    ~Joiner() { if (t.joinable()) t.join(); }
+  } joiner{fro};
   if (fast) {
-    std::vector<ff::F> sq(Af.size());
-    par_rows(Af.size(), threads, [&](size_t a, size_t b) {
-      for (size_t e = a; e < b; ++e) sq[e] = ff::mul(Af[e], Af[e], pi);
+    fro = std::thread([&] {
+      ff::F acc;
+      for (int t = 0; t < T; ++t) {
+        const size_t a = nn * t / T, b = nn * (t + 1) / T;
+        for (size_t e = a; e < b; ++e) {
+          while (done[t].load(std::memory_order_acquire) <= e - a) {
+            if (abort_sum.load()) return;
+            std::this_thread::yield();
+          }
+          acc = ff::fadd(acc, Sq[e], pi);
+        }
+      }
+      fro_acc = acc;
     });
-    ff::F acc;
-    for (const ff::F &v : sq) acc = ff::add(acc, v, pi);
-    a_fro = lf_sqrt(ff::to_bf(acc), p);
+    // one pass: fixed-width copy, its square and its k binary64 heads
+    // (bf_to_multicomp)
+    std::vector<char> bad(T, 0);
+    std::vector<std::thread> ws;
+    for (int t = 0; t < T; ++t)
+      ws.emplace_back([&, t] {
+        const size_t a = nn * t / T, b = nn * (t + 1) / T;
+        double c[4];
+        for (size_t e = a; e < b; ++e) {
+          const ff::F v = ff::from_bf(Avals[e], pi);
+          Af[e] = v;
+          Sq[e] = ff::fmul(v, v, pi);
+          if (!ff::to_multicomp(v, k, pi, c) &&
+              bn::to_multicomp(Avals[e], k, c)) {
+            bad[t] = 1;
+            break;
+          }
+          for (int q = 0; q < k; ++q) a_pl[(size_t)q * nn + e] = c[q];
+          if ((e - a) % 512 == 511)
+            done[t].store(e - a + 1, std::memory_order_release);
+        }
+        done[t].store(b - a, std::memory_order_release);
+      });
+    for (auto &w : ws) w.join();
+    for (int t = 0; t < T; ++t)
+      if (bad[t]) {
+        abort_sum.store(true);
+        err = "value does not fit in binary64";
+        return 5;
+      }
   } else {
+    if ((st = to_planes(Avals, k, a_pl.p, nn, err, threads))) return st;
     std::vector<BF> sq(Avals.size());
     par_rows(Avals.size(), threads, [&](size_t a, size_t b) {
       for (size_t e = a; e < b; ++e) sq[e] = lf_mul(Avals[e], Avals[e], p);
@@ -395,13 +455,72 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
     for (const BF &s : sq) acc = lf_add(acc, s, p);
     a_fro = lf_sqrt(acc, p);
   }
+  plog.mark("A -> fixed, planes");
+  if ((st = to_planes(Bvals, k, b_pl.data(), (size_t)n, err))) return st;
+  const auto t1 = Clock::now();
+  if ((st = S.factor(k, n, a_pl.p, err))) return st;
+  const auto t2 = Clock::now();
+  plog.mark("factor");
+  double t_solve = 0, t_res = 0;
+  auto timed_solve = [&](const std::vector<double> &rhs) {
+    const auto a = Clock::now();
+    const int r = S.solve(rhs, x_pl, err);
+    t_solve += secs(a, Clock::now());
+    return r;
+  };
+  if ((st = timed_solve(b_pl))) return st;
+  plog.mark("first solve");
+  // bf_from_multicomp at p_in, then into the working precision
+  auto lift = [&](const std::vector<double> &pl, std::vector<BF> &x) {
+    x.resize(n);
+    double c[4];
+    for (int i = 0; i < n; ++i) {
+      for (int q = 0; q < k; ++q) c[q] = pl[(size_t)q * n + i];
+      x[i] = lf_round(from_components(c, k, p_in), p);
+    }
+  };
+  // the same on fixed-width values: the components are summed at p_in,
+  // exactly whenever they span fewer than p_in - 56 bits (always, for the
+  // renormalised values the GPU returns); otherwise the generic path
+  const int pin = (int)p_in;
+  auto lift_f = [&](const std::vector<double> &pl, std::vector<ff::F> &x) {
+    x.resize(n);
+    for (int i = 0; i < n; ++i) {
+      double c[4];
+      int emax = INT_MIN, emin = INT_MAX;
+      for (int q = 0; q < k; ++q) {
+        c[q] = pl[(size_t)q * n + i];
+        if (c[q] != 0.0) {
+          const int e = std::ilogb(c[q]);
+          emax = std::max(emax, e);
+          emin = std::min(emin, e);
+        }
+      }
+      if (emax != INT_MIN && emax - emin > pin - 56) {
+        x[i] = ff::from_bf(lf_round(from_components(c, k, p_in), p), pi);
+        continue;
+      }
+      ff::F acc;
+      for (int q = 0; q < k; ++q)
+        if (c[q] != 0.0) acc = ff::fadd(acc, ff::from_double(c[q], pin), pin);
+      x[i] = ff::round(acc, pin, pi);
+    }
+  };
+  std::vector<BF> x;
+  std::vector<ff::F> xf, resf, zf, Bf;
+  if (fast) {
+    lift_f(x_pl, xf);
+    Bf.resize(n);
+    for (int i = 0; i < n; ++i) Bf[i] = ff::from_bf(Bvals[i], pi);
+  } else {
+    lift(x_pl, x);
+  }
+  plog.mark("lift x");
   const BF one = from_int(1, p);
-  // check_stop threshold factor sqrt(n) * rtol * a_fro, left to right
   std::vector<BF> res(n), work(n), z;
-  std::vector<ff::F> xf, resf;
   auto norm2_f = [&](const std::vector<ff::F> &v) {
     ff::F acc;
-    for (const ff::F &s : v) acc = ff::add(acc, ff::mul(s, s, pi), pi);
+    for (const ff::F &s : v) acc = ff::fadd(acc, ff::fmul(s, s, pi), pi);
     return lf_sqrt(ff::to_bf(acc), p);
   };
   std::string reason = "max_iter";
@@ -412,22 +531,24 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
     const auto ta = Clock::now();
     BF res_norm, x_norm;
     if (fast) {
-      xf.resize(n);
-      for (int i = 0; i < n; ++i) xf[i] = ff::from_bf(x[i], pi);
       resf.resize(n);
       par_rows((size_t)n, threads, [&](size_t r0, size_t r1) {
         for (size_t i = r0; i < r1; ++i) {
           ff::F acc;
           const ff::F *row = &Af[i * n];
           for (int j = 0; j < n; ++j)
-            acc = ff::add(acc, ff::mul(row[j], xf[j], pi), pi);
-          resf[i] = ff::add(Bf[i], ff::neg(acc), pi);
+            acc = ff::fadd(acc, ff::fmul(row[j], xf[j], pi), pi);
+          resf[i] = ff::fadd(Bf[i], ff::neg(acc), pi);
         }
       });
       t_res += secs(ta, Clock::now());
-      for (int i = 0; i < n; ++i) res[i] = ff::to_bf(resf[i]);
       res_norm = norm2_f(resf);
       x_norm = norm2_f(xf);
+      if (fro.joinable()) {
+        fro.join();
+        a_fro = lf_sqrt(ff::to_bf(fro_acc), p);
+        plog.mark("||A||_F (join)");
+      }
     } else {
       par_rows((size_t)n, threads, [&](size_t r0, size_t r1) {
         for (size_t i = r0; i < r1; ++i) {
@@ -442,6 +563,7 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
       res_norm = norm2(res, p);
       x_norm = norm2(x, p);
     }
+    plog.mark("residual + norms");
     out.residuals.push_back(res_norm);
     if (res_norm.sign == 0) { reason = "converged"; break; }
     BF t = lf_sqrt(from_int(n, p), p);
@@ -457,14 +579,44 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
       reason = "stagnated";
       break;
     }
+    // z = solve(r / ||r||), x += z * ||r||  (refine.py:184-190)
     BF coef = lf_div(one, res_norm, p);
-    for (int i = 0; i < n; ++i) work[i] = lf_mul(res[i], coef, p);
-    std::vector<double> w_pl;
-    if ((st = to_planes(work, k, w_pl, (size_t)n, err))) return st;
+    std::vector<double> w_pl((size_t)k * n);
+    if (fast) {
+      const ff::F cf = ff::from_bf(coef, pi);
+      for (int i = 0; i < n; ++i) {
+        const ff::F w = ff::fmul(resf[i], cf, pi);
+        double c[4];
+        if (!ff::to_multicomp(w, k, pi, c) &&
+            bn::to_multicomp(ff::to_bf(w), k, c)) {
+          err = "value does not fit in binary64";
+          return 5;
+        }
+        for (int q = 0; q < k; ++q) w_pl[(size_t)q * n + i] = c[q];
+      }
+    } else {
+      for (int i = 0; i < n; ++i) work[i] = lf_mul(res[i], coef, p);
+      if ((st = to_planes(work, k, w_pl.data(), (size_t)n, err))) return st;
+    }
     if ((st = timed_solve(w_pl))) return st;
-    lift(x_pl, z);
-    for (int i = 0; i < n; ++i) x[i] = lf_add(x[i], lf_mul(z[i], res_norm, p), p);
+    if (fast) {
+      lift_f(x_pl, zf);
+      const ff::F rn = ff::from_bf(res_norm, pi);
+      for (int i = 0; i < n; ++i)
+        xf[i] = ff::fadd(xf[i], ff::fmul(zf[i], rn, pi), pi);
+    } else {
+      lift(x_pl, z);
+      for (int i = 0; i < n; ++i) x[i] = lf_add(x[i], lf_mul(z[i], res_norm, p), p);
+    }
     ++corrections;
+    plog.mark("correction");
+  }
+  if (fro.joinable()) {  // (stopped before the first check)
+    fro.join();
+  }
+  if (fast) {
+    x.resize(n);
+    for (int i = 0; i < n; ++i) x[i] = ff::to_bf(xf[i]);
   }
   const auto t3 = Clock::now();
   out.iterations = corrections;
@@ -524,6 +676,39 @@ int64_t longfloat_selftest(int64_t iters, uint64_t seed, int p) {
     if (lf_cmp(s, s_ref) != 0 || s.sign != s_ref.sign) ++bad;
     if (lf_cmp(d, d_ref) != 0 || d.sign != d_ref.sign) ++bad;
     if (lf_cmp(mm, m_ref) != 0 || mm.sign != m_ref.sign) ++bad;
+    // the compile-time-width kernels (fadd / fmul) on the same operands
+    const BF s2 = ff::to_bf(ff::fadd(fa, fb, p));
+    const BF d2 = ff::to_bf(ff::fadd(fa, ff::neg(fb), p));
+    const BF m2 = ff::to_bf(ff::fmul(fa, fb, p));
+    if (lf_cmp(s2, s_ref) != 0 || s2.sign != s_ref.sign) ++bad;
+    if (lf_cmp(d2, d_ref) != 0 || d2.sign != d_ref.sign) ++bad;
+    if (lf_cmp(m2, m_ref) != 0 || m2.sign != m_ref.sign) ++bad;
+    // bf_to_multicomp on the fixed-width value (when it takes the fast path)
+    for (int k = 2; k <= 4; ++k) {
+      double c1[4], c2[4];
+      if (ff::to_multicomp(fa, k, p, c1)) {
+        if (bn::to_multicomp(a, k, c2) != 0 ||
+            std::memcmp(c1, c2, sizeof(double) * k) != 0)
+          ++bad;
+      }
+    }
+    // the lift of k binary64 components: exact sum at p + 64, then p
+    if (p + 64 <= 64 * ff::NL) {
+      double c[4];
+      if (bn::to_multicomp(a, 4, c) == 0) {
+        const int pin = p + 64;
+        ff::F acc;
+        BF ex;
+        for (int q = 0; q < 4; ++q) {
+          if (c[q] == 0.0) continue;
+          acc = ff::fadd(acc, ff::from_double(c[q], pin), pin);
+          ex = bn::add_exact(ex, bn::from_binary64(c[q]));
+        }
+        const BF l1 = ff::to_bf(ff::round(acc, pin, p));
+        const BF l2 = lf_round(lf_round(ex, pin), p);
+        if (lf_cmp(l1, l2) != 0 || l1.sign != l2.sign) ++bad;
+      }
+    }
   }
   return bad;
 }

@@ -29,7 +29,7 @@ class ShortSolver {
  public:
   virtual ~ShortSolver() = default;
   // -> status (0 ok, 3 singular, 6 other)
-  virtual int factor(int k, int n, const std::vector<double> &a_planes,
+  virtual int factor(int k, int n, const double *a_planes,
                      std::string &err) = 0;
   virtual int solve(const std::vector<double> &b_planes,
                     std::vector<double> &x_planes, std::string &err) = 0;

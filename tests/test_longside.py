@@ -105,7 +105,7 @@ def test_refinement_matches_reference(monkeypatch, idx):
     assert [format_hex(x) for x in rep.solution.data] == case["solution"]
 
 
-@pytest.mark.parametrize("prec", [53, 106, 424, 512, 640])
+@pytest.mark.parametrize("prec", [53, 64, 65, 106, 300, 424, 512, 576, 640])
 def test_fixed_width_long_arithmetic_matches_generic(prec):
     # the refinement loop's fixed-width add/sub/mul (fastfloat.h) against
     # the generic big-integer path (bigfloat.py single-rounding semantics)
