@@ -243,6 +243,11 @@ int32_t mpcore_prof_read(double *ms, int64_t *launches, int32_t cap);
 /* diagnostics: per-CTA, per-column phase timestamps (ns) of the panel
  * selected by the MPCORE_TRACE_PANEL environment variable; [SMs][32][8] */
 int32_t mpcore_debug_panel_trace(uint64_t *out_ns, int64_t cap);
+/* Diagnostics: per-panel kernel entry/exit stamps (globaltimer ns) of the
+   next LUs.  out == NULL arms / resets a len-entry buffer (4 per column
+   index J: panel entry, panel exit, exchange+U12 entry, exit); otherwise
+   copies len entries to out.  Extension (no reference counterpart). */
+int32_t mpcore_debug_lu_stamps(int64_t len, uint64_t *out);
 /* diagnostics: owner timestamps (ns) of every row block of the last solve
  * (MPCORE_TRACE_SOLVE set): [forward, backward][blocks][4] = start, completed
  * source blocks added, critical source block done, diagonal done */

@@ -71,6 +71,7 @@ _PROTOS = {
     "mpcore_prof_read": (_i32, [_dp, ctypes.POINTER(_i64), _i32]),
     "mpcore_fp64_peak": (_i32, [_dp, _dp]),
     "mpcore_debug_panel_trace": (_i32, [ctypes.POINTER(_u64), _i64]),
+    "mpcore_debug_lu_stamps": (_i32, [_i64, ctypes.POINTER(_u64)]),
     "mpcore_solve_system": (_i32, [_u64, _u64, _u64, _i32, ctypes.POINTER(_u64),
                                    ctypes.POINTER(_i32)]),
     "mpcore_dev_solve_system": (_i32, [_i32, _i32, _u64, _i64, _i64, _i32,

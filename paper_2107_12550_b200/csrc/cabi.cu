@@ -1232,6 +1232,40 @@ int32_t mpcore_debug_timeline(double *out, int64_t cap, int64_t *count) {
   return MPCORE_OK;
 }
 
+// MPCORE_LU_STAMPS diagnostics: out == NULL (re)arms a buffer of len
+// entries (4 per column index: panel entry/exit, exchange+U12 entry/exit,
+// globaltimer ns; unset entries ~0 / 0); otherwise copies len entries out.
+int32_t mpcore_debug_lu_stamps(int64_t len, uint64_t *out) {
+  DevLock L;
+  if (L.st) return L.st;
+  static unsigned long long *buf = nullptr;
+  static int64_t cap = 0;
+  if (len <= 0 || len % 4) return MPCORE_BAD_DIMENSION;
+  cudaError_t e;
+  if (out == nullptr) {
+    if (len > cap) {
+      if (buf) cudaFree(buf);
+      buf = nullptr;
+      cap = 0;
+      if ((e = cudaMalloc(&buf, len * 8)) != cudaSuccess)
+        return cuda_fail(e, "stamps");
+      cap = len;
+    }
+    std::vector<unsigned long long> init((size_t)len);
+    for (int64_t i = 0; i < len; ++i) init[i] = (i % 2 == 0) ? ~0ull : 0ull;
+    if ((e = cudaMemcpy(buf, init.data(), len * 8, cudaMemcpyHostToDevice)) !=
+            cudaSuccess ||
+        (e = mpk::lu_stamps_enable(buf)) != cudaSuccess)
+      return cuda_fail(e, "stamps");
+    return MPCORE_OK;
+  }
+  if (!buf || len > cap) return MPCORE_BAD_DIMENSION;
+  if ((e = cudaMemcpy(out, buf, len * 8, cudaMemcpyDeviceToHost)) !=
+      cudaSuccess)
+    return cuda_fail(e, "stamps");
+  return MPCORE_OK;
+}
+
 int32_t mpcore_debug_panel_trace(uint64_t *out_ns, int64_t cap) {
   DevLock L;
   if (L.st) return L.st;

@@ -50,6 +50,8 @@ struct LuWork {
 };
 
 int num_sms();
+// diagnostics: per-panel kernel stamps into buf ([4 * n] u64) or off (null)
+cudaError_t lu_stamps_enable(unsigned long long *buf);
 
 // elementwise op: 0 add(x,y), 1 mul(x,y), 2 div(x,y); n lanes, planar
 cudaError_t elementwise(int k, int op, int64_t n, const double *x,

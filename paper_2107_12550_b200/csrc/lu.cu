@@ -77,6 +77,22 @@ __device__ __forceinline__ unsigned long long mag_key(double m) {
   return b > 0x7FF0000000000000ull ? 0x7FF8000000000000ull : b;
 }
 
+// diagnostics (MPCORE_LU_STAMPS): per column index J, globaltimer at the
+// first CTA entry / last CTA exit of the panel and exchange+U12 kernels:
+// [0] panel entry (min) [1] panel exit (max) [2] swap_trsm entry (min)
+// [3] swap_trsm exit (max); null when disabled
+__device__ unsigned long long *g_lu_stamps = nullptr;
+__device__ __forceinline__ void lu_stamp(int J, int slot, bool is_min) {
+  unsigned long long *st = g_lu_stamps;
+  if (st == nullptr) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (is_min)
+    atomicMin(st + 4 * (int64_t)J + slot, t);
+  else
+    atomicMax(st + 4 * (int64_t)J + slot, t);
+}
+
 #include "panel.cuh"
 
 // diagnostics: globaltimer into a trace slot (around the traced panel)
@@ -191,6 +207,7 @@ swap_trsm_kernel(MatView A, int J, int w, int c0, int c1, int c2, int c3,
   // lane -- the triangle's shrinking work stays balanced, so a warp does
   // 46 madd steps for two columns instead of 62)
   constexpr int CPW = 32 / LPC, CPB = 4 * CPW, NE = 2 * LU_MAX_W / LPC;
+  if (threadIdx.x == 0) lu_stamp(J, 2, true);
   if (status[0] >= 0) return;
   __shared__ int cur[2 * LU_MAX_W], src[2 * LU_MAX_W], rsrc[LU_MAX_W];
   __shared__ double Ls[K][LU_MAX_W][LU_MAX_W + 1];
@@ -314,6 +331,7 @@ swap_trsm_kernel(MatView A, int J, int w, int c0, int c1, int c2, int c3,
         pc[k * A.plane + (int64_t)cur[sl + LPC * q] * ld] = v[q][k];
     }
   }
+  if (threadIdx.x == 0) lu_stamp(J, 3, false);
 }
 
 template <typename... KArgs, typename... Args>
@@ -588,6 +606,10 @@ cudaError_t LuWork::init(int sms) {
           cudaSuccess)
     return e;
   return cudaDeviceSynchronize();
+}
+
+cudaError_t lu_stamps_enable(unsigned long long *buf) {
+  return cudaMemcpyToSymbol(g_lu_stamps, &buf, sizeof(buf));
 }
 
 cudaError_t lu_begin(LuWork &ws, cudaStream_t s) {

@@ -70,6 +70,7 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
              LuWork ws, int slot) {
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31;
+  if (tid == 0) lu_stamp(J, 0, true);
   if (ws.status[0] >= 0) return;
   if (ws.trace != nullptr && ws.trace_J == J && tid == 0) {
     unsigned long long t;
@@ -435,4 +436,5 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
     if (lane == 0) sl[4 * LU_MAX_W] = __popc(ma) + __popc(mb);
   }
   stamp(3);
+  if (tid == 0) lu_stamp(J, 1, false);
 }
