@@ -248,6 +248,11 @@ int32_t mpcore_debug_panel_trace(uint64_t *out_ns, int64_t cap);
    index J: panel entry, panel exit, exchange+U12 entry, exit); otherwise
    copies len entries to out.  Extension (no reference counterpart). */
 int32_t mpcore_debug_lu_stamps(int64_t len, uint64_t *out);
+/* Device timing on the library's stream (all compute and copies run there):
+   record CUDA event `slot` (0..7); elapsed milliseconds from slot a to slot
+   b (waits for b).  Extension (bench.py). */
+int32_t mpcore_stream_event_record(int32_t slot);
+int32_t mpcore_stream_event_elapsed(int32_t a, int32_t b, double *ms);
 /* diagnostics: owner timestamps (ns) of every row block of the last solve
  * (MPCORE_TRACE_SOLVE set): [forward, backward][blocks][4] = start, completed
  * source blocks added, critical source block done, diagonal done */

@@ -72,6 +72,8 @@ _PROTOS = {
     "mpcore_fp64_peak": (_i32, [_dp, _dp]),
     "mpcore_debug_panel_trace": (_i32, [ctypes.POINTER(_u64), _i64]),
     "mpcore_debug_lu_stamps": (_i32, [_i64, ctypes.POINTER(_u64)]),
+    "mpcore_stream_event_record": (_i32, [_i32]),
+    "mpcore_stream_event_elapsed": (_i32, [_i32, _i32, ctypes.POINTER(ctypes.c_double)]),
     "mpcore_solve_system": (_i32, [_u64, _u64, _u64, _i32, ctypes.POINTER(_u64),
                                    ctypes.POINTER(_i32)]),
     "mpcore_dev_solve_system": (_i32, [_i32, _i32, _u64, _i64, _i64, _i32,
@@ -314,3 +316,24 @@ def sm_count():
 
 def sync():
     check(lib().mpcore_sync(), "sync")
+
+
+class StreamTimer:
+    """Device time between start() and stop(): CUDA events recorded on the
+    library's stream (every kernel and host<->device copy of libmpcore runs
+    there), slots a and b of mpcore_stream_event_record."""
+
+    def __init__(self, a=0, b=1):
+        self.a, self.b = a, b
+
+    def start(self):
+        check(lib().mpcore_stream_event_record(self.a), "event record")
+
+    def stop(self):
+        """-> elapsed milliseconds (waits for the stop event)."""
+        check(lib().mpcore_stream_event_record(self.b), "event record")
+        ms = ctypes.c_double()
+        check(lib().mpcore_stream_event_elapsed(self.a, self.b,
+                                                ctypes.byref(ms)),
+              "event elapsed")
+        return ms.value

@@ -181,6 +181,11 @@ int ensure_device_locked() {
   return MPCORE_OK;
 }
 
+cudaEvent_t *event_slots() {
+  static cudaEvent_t slots[8] = {};
+  return slots;
+}
+
 struct DevLock {
   std::unique_lock<std::mutex> lk;
   int st;
@@ -1229,6 +1234,33 @@ int32_t mpcore_debug_timeline(double *out, int64_t cap, int64_t *count) {
   if (out) {
     for (int64_t i = 0; i < n && i < cap; ++i) out[i] = P.timeline[i];
   }
+  return MPCORE_OK;
+}
+
+// Device timing on the library stream: CUDA events in 8 slots.
+int32_t mpcore_stream_event_record(int32_t slot) {
+  DevLock L;
+  if (L.st) return L.st;
+  static cudaEvent_t ev[8] = {};
+  if (slot < 0 || slot >= 8) return MPCORE_BAD_DIMENSION;
+  cudaError_t e = cudaSuccess;
+  if (!ev[slot]) e = cudaEventCreate(&ev[slot]);
+  if (e == cudaSuccess) e = cudaEventRecord(ev[slot], device().stream);
+  if (e != cudaSuccess) return cuda_fail(e, "event record");
+  event_slots()[slot] = ev[slot];
+  return MPCORE_OK;
+}
+
+int32_t mpcore_stream_event_elapsed(int32_t a, int32_t b, double *ms) {
+  if (ms == nullptr || a < 0 || a >= 8 || b < 0 || b >= 8)
+    return MPCORE_BAD_DIMENSION;
+  cudaEvent_t ea = event_slots()[a], eb = event_slots()[b];
+  if (!ea || !eb) return MPCORE_BAD_DIMENSION;
+  cudaError_t e = cudaEventSynchronize(eb);
+  float f = 0.0f;
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&f, ea, eb);
+  if (e != cudaSuccess) return cuda_fail(e, "event elapsed");
+  *ms = f;
   return MPCORE_OK;
 }
 
