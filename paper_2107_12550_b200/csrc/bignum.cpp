@@ -178,7 +178,20 @@ void UBig::divmod(const UBig &a, const UBig &b, UBig &q, UBig &r) {
 
 UBig UBig::isqrt(const UBig &a) {
   if (a.zero()) return UBig();
-  UBig x = UBig(1).shl((a.bits() + 1) / 2 + 1);
+  // Newton from above converges to floor(sqrt(a)) from any start >=
+  // sqrt(a); start from the binary64 root of the leading bits (rounded up
+  // with margin), so a few iterations suffice instead of ~log2(bits)
+  const int64_t nb = a.bits();
+  UBig x;
+  if (nb > 64) {
+    int64_t sh = nb - 62;
+    if (sh & 1) sh += 1;                       // even: sqrt(2^sh) exact
+    const uint64_t top = a.shr(sh).low64();    // a < (top + 1) 2^sh
+    const double r = std::sqrt((double)top + 2.0) * (1.0 + 0x1p-40) + 2.0;
+    x = UBig((uint64_t)std::ceil(r)).shl(sh / 2);
+  } else {
+    x = UBig(1).shl((nb + 1) / 2 + 1);
+  }
   for (;;) {
     UBig q, r;
     divmod(a, x, q, r);

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <chrono>
@@ -23,6 +24,7 @@
 #include "../../include/mpcore.h"
 #include "bignum.h"
 #include "internal.h"
+#include "longfloat.cuh"
 #include "refine_host.h"
 #include "testsys.h"
 
@@ -604,7 +606,38 @@ struct IrWorkspace {
   double *a = nullptr, *b = nullptr, *x = nullptr;
   int32_t *perm = nullptr;
   size_t acap = 0, bcap = 0, xcap = 0, pcap = 0;
+  // the long residual (residual.cu): page-locked staging of the
+  // fixed-width A, its device copy, vectors, and the upload stream
+  void *stage = nullptr, *hx = nullptr, *hres = nullptr;
+  size_t stagecap = 0, hcap = 0;
+  void *rA = nullptr, *rb = nullptr, *rx = nullptr, *rres = nullptr;
+  size_t rAcap = 0, rbcap = 0, rxcap = 0, rrcap = 0;
+  cudaStream_t up = nullptr;
+  cudaEvent_t up_done = nullptr;
 };
+// (the host's ff::F, uploaded as is)
+static_assert(sizeof(lf::DF) == 96 && offsetof(lf::DF, exp) == 8 &&
+                  offsetof(lf::DF, m) == 16,
+              "lf::DF layout must match ff::F");
+constexpr size_t LF_BYTES = sizeof(lf::DF);
+cudaError_t grow_dev(void **p, size_t &cap, size_t need) {
+  if (cap >= need) return cudaSuccess;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  cap = 0;
+  cudaError_t r = cudaMalloc(p, need);
+  if (r == cudaSuccess) cap = need;
+  return r;
+}
+cudaError_t grow_host(void **p, size_t &cap, size_t need) {
+  if (cap >= need) return cudaSuccess;
+  if (*p) cudaFreeHost(*p);
+  *p = nullptr;
+  cap = 0;
+  cudaError_t r = cudaHostAlloc(p, need, cudaHostAllocDefault);
+  if (r == cudaSuccess) cap = need;
+  return r;
+}
 IrWorkspace &ir_ws() {
   static IrWorkspace w;
   return w;
@@ -635,25 +668,12 @@ class GpuShortSolver : public mpr::ShortSolver {
     Device &D = device();
     cudaError_t e = cudaSuccess;
     size_t mb = (size_t)k * n * n * sizeof(double), vb = (size_t)k * n * 8;
-    bool expected = false;
-    if (!shared_ && a_ == nullptr &&
-        ir_ws().busy.compare_exchange_strong(expected, true))
-      shared_ = true;
-    if (shared_) {
+    if (a_ == nullptr && claim()) {
       IrWorkspace &w = ir_ws();
-      auto grow = [&](void **p, size_t &cap, size_t need) {
-        if (cap >= need) return cudaSuccess;
-        if (*p) cudaFree(*p);
-        *p = nullptr;
-        cap = 0;
-        cudaError_t r = cudaMalloc(p, need);
-        if (r == cudaSuccess) cap = need;
-        return r;
-      };
-      if ((e = grow((void **)&w.a, w.acap, mb)) == cudaSuccess &&
-          (e = grow((void **)&w.b, w.bcap, vb)) == cudaSuccess &&
-          (e = grow((void **)&w.x, w.xcap, vb)) == cudaSuccess)
-        e = grow((void **)&w.perm, w.pcap, (size_t)n * 4);
+      if ((e = grow_dev((void **)&w.a, w.acap, mb)) == cudaSuccess &&
+          (e = grow_dev((void **)&w.b, w.bcap, vb)) == cudaSuccess &&
+          (e = grow_dev((void **)&w.x, w.xcap, vb)) == cudaSuccess)
+        e = grow_dev((void **)&w.perm, w.pcap, (size_t)n * 4);
       if (e != cudaSuccess) {
         err = cudaGetErrorString(e);
         return MPCORE_INTERNAL;
@@ -662,10 +682,11 @@ class GpuShortSolver : public mpr::ShortSolver {
       b_ = w.b;
       x_ = w.x;
       perm_ = w.perm;
-    } else if ((e = cudaMalloc(&a_, mb)) != cudaSuccess ||
+    } else if (a_ == nullptr &&
+               ((e = cudaMalloc(&a_, mb)) != cudaSuccess ||
                (e = cudaMalloc(&b_, vb)) != cudaSuccess ||
                (e = cudaMalloc(&x_, vb)) != cudaSuccess ||
-               (e = cudaMalloc(&perm_, (size_t)n * 4)) != cudaSuccess) {
+               (e = cudaMalloc(&perm_, (size_t)n * 4)) != cudaSuccess)) {
       err = cudaGetErrorString(e);
       return MPCORE_INTERNAL;
     }
@@ -696,6 +717,75 @@ class GpuShortSolver : public mpr::ShortSolver {
     (void)D;
     return MPCORE_OK;
   }
+  // ---- the long residual on the device (residual.cu) ----
+  bool residual_supported(int p) override { return p <= 512 && claim(); }
+  void *staging(size_t bytes) override {
+    if (!claim()) return nullptr;
+    DevLock L;
+    if (L.st) return nullptr;
+    IrWorkspace &w = ir_ws();
+    if (grow_host(&w.stage, w.stagecap, bytes) != cudaSuccess) return nullptr;
+    return w.stage;
+  }
+  int residual_setup(int n, int p, const void *A, const void *b,
+                     std::string &err) override {
+    DevLock L;
+    if (L.st) { err = g_err; return L.st; }
+    if (!shared_) { err = "no residual workspace"; return MPCORE_INTERNAL; }
+    IrWorkspace &w = ir_ws();
+    const size_t mb = (size_t)n * n * LF_BYTES, vb = (size_t)n * LF_BYTES;
+    cudaError_t e = cudaSuccess;
+    if (!w.up) {
+      if ((e = cudaStreamCreateWithFlags(&w.up, cudaStreamNonBlocking)) ==
+          cudaSuccess)
+        e = cudaEventCreateWithFlags(&w.up_done, cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = grow_dev(&w.rA, w.rAcap, mb);
+    if (e == cudaSuccess) e = grow_dev(&w.rb, w.rbcap, vb);
+    if (e == cudaSuccess) e = grow_dev(&w.rx, w.rxcap, vb);
+    if (e == cudaSuccess) e = grow_dev(&w.rres, w.rrcap, vb);
+    if (e == cudaSuccess) e = grow_host(&w.hx, w.hcap, 2 * vb);
+    if (e == cudaSuccess && A != w.stage) e = cudaErrorInvalidValue;
+    // A from the page-locked staging: asynchronous, overlapping the LU
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(w.rA, A, mb, cudaMemcpyHostToDevice, w.up);
+    if (e == cudaSuccess) {
+      std::memcpy(w.hx, b, vb);
+      e = cudaMemcpyAsync(w.rb, w.hx, vb, cudaMemcpyHostToDevice, w.up);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(w.up_done, w.up);
+    if (e != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
+    rn_ = n;
+    rp_ = p;
+    return MPCORE_OK;
+  }
+  int residual(const void *x, void *res, std::string &err) override {
+    DevLock L;
+    if (L.st) { err = g_err; return L.st; }
+    IrWorkspace &w = ir_ws();
+    Device &D = device();
+    const size_t vb = (size_t)rn_ * LF_BYTES;
+    char *hx = static_cast<char *>(w.hx), *hres = hx + vb;
+    std::memcpy(hx, x, vb);
+    cudaError_t e = cudaMemcpyAsync(w.rx, hx, vb, cudaMemcpyHostToDevice,
+                                    D.stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(D.stream, w.up_done, 0);
+    if (e == cudaSuccess)
+      e = mpk::long_residual(rp_, rn_, w.rA, w.rx, w.rb, w.rres, D.stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(hres, w.rres, vb, cudaMemcpyDeviceToHost, D.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(D.stream);
+    if (e != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
+    std::memcpy(res, hres, vb);
+    return MPCORE_OK;
+  }
+
   int solve(const std::vector<double> &b, std::vector<double> &x,
             std::string &err) override {
     DevLock L;
@@ -719,7 +809,17 @@ class GpuShortSolver : public mpr::ShortSolver {
   }
 
  private:
-  int k_ = 0, n_ = 0;
+  // the shared workspace, if no other refinement holds it (asked once)
+  bool claim() {
+    if (!tried_) {
+      tried_ = true;
+      bool expected = false;
+      shared_ = ir_ws().busy.compare_exchange_strong(expected, true);
+    }
+    return shared_;
+  }
+  int k_ = 0, n_ = 0, rn_ = 0, rp_ = 0;
+  bool tried_ = false;
   bool shared_ = false;  // buffers borrowed from ir_ws()
   double *a_ = nullptr, *b_ = nullptr, *x_ = nullptr;
   int32_t *perm_ = nullptr;
@@ -1309,6 +1409,16 @@ int32_t mpcore_debug_panel_trace(uint64_t *out_ns, int64_t cap) {
                              cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(e, "trace");
   return MPCORE_OK;
+}
+
+int32_t mpcore_debug_long_residual_selftest(int32_t n, int32_t prec,
+                                            uint64_t seed,
+                                            int64_t *mismatches) {
+  if (!mismatches) return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  *mismatches = mpr::long_residual_selftest(n, prec, seed, device().stream);
+  return *mismatches < 0 ? MPCORE_INTERNAL : MPCORE_OK;
 }
 
 int32_t mpcore_debug_longfloat_selftest(int64_t iters, uint64_t seed,

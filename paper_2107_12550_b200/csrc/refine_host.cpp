@@ -7,12 +7,14 @@
 // The short factorisation and every correction solve run on the GPU through
 // ShortSolver (cabi.cu).
 #include "refine_host.h"
+#include "internal.h"
 
 #include "fastfloat.h"
 
 #include <algorithm>
 #include <atomic>
 #include <climits>
+#include <cstddef>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -310,14 +312,23 @@ static int to_planes(const std::vector<BF> &v, int k, double *out,
 // threads); alloc() -> false when out of memory
 template <class T> struct RawBuf {
   T *p = nullptr;
+  bool owned = false;
   bool alloc(size_t n) {
     p = static_cast<T *>(std::malloc(n * sizeof(T) + 1));
-    return p != nullptr;
+    owned = p != nullptr;
+    return owned;
   }
+  void adopt(T *ext) { p = ext; }   // memory owned elsewhere
   T &operator[](size_t i) { return p[i]; }
   const T &operator[](size_t i) const { return p[i]; }
-  ~RawBuf() { std::free(p); }
+  ~RawBuf() {
+    if (owned) std::free(p);
+  }
 };
+// the device residual takes the host layout unchanged (longfloat.cuh DF)
+static_assert(sizeof(ff::F) == 96 && offsetof(ff::F, exp) == 8 &&
+                  offsetof(ff::F, m) == 16,
+              "ff::F layout must match lf::DF");
 
 static BF norm2(const std::vector<BF> &v, int64_t p) {
   BF acc;
@@ -376,47 +387,42 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
   // n x n buffers are first touched by the threads that fill them (a
   // zero-filled std::vector would page them in on one thread)
   RawBuf<double> a_pl;
-  RawBuf<ff::F> Af, Sq;
+  RawBuf<ff::F> Af;
+  // the residual on the GPU when the short side offers it (p <= 512): the
+  // fixed-width A is then written straight into its page-locked staging
+  const bool dev_res = fast && S.residual_supported(pi);
+  if (dev_res) {
+    if (void *st_buf = S.staging(nn * sizeof(ff::F)))
+      Af.adopt(static_cast<ff::F *>(st_buf));
+  }
   if (!a_pl.alloc((size_t)k * nn) ||
-      (fast && (!Af.alloc(nn) || !Sq.alloc(nn)))) {
+      (fast && Af.p == nullptr && !Af.alloc(nn))) {
     err = "out of host memory";
     return 6;
   }
   std::vector<double> b_pl((size_t)k * n), x_pl;
-  // ||A||_F, row-major accumulation (linalg.py:692-700): the squares are
-  // formed by the conversion pass on all threads; their sum, sequential in
-  // the reference's order, runs on its own thread, following the pass
-  // (per-worker progress counters) and then overlapping the GPU factor and
-  // the first solve
+  // ||A||_F, row-major accumulation (linalg.py:692-700).  check_stop only
+  // compares against a threshold monotone in ||A||_F, so rigorous bounds
+  // from the binary64 heads (below) decide every comparison that does not
+  // land within ~2^-40 (relative) of the threshold; the exact, sequentially
+  // rounded sum is formed only for one that does (exact_fro).
   BF a_fro;
-  ff::F fro_acc;
-  // (declared before the thread: they outlive its join)
   const int T = (int)std::max<size_t>(1, std::min<size_t>((size_t)threads, nn));
-  std::unique_ptr<std::atomic<size_t>[]> done(new std::atomic<size_t>[T]);
-  std::atomic<bool> abort_sum{false};
-  for (int t = 0; t < T; ++t) done[t].store(0);
-  std::thread fro;
-  struct Joiner {  // every return below joins the summing thread
-    std::thread &t;
-    ~Joiner() { if (t.joinable()) t.join(); }
-  } joiner{fro};
-  if (fast) {
-    fro = std::thread([&] {
-      ff::F acc;
-      for (int t = 0; t < T; ++t) {
-        const size_t a = nn * t / T, b = nn * (t + 1) / T;
-        for (size_t e = a; e < b; ++e) {
-          while (done[t].load(std::memory_order_acquire) <= e - a) {
-            if (abort_sum.load()) return;
-            std::this_thread::yield();
-          }
-          acc = ff::fadd(acc, Sq[e], pi);
-        }
-      }
-      fro_acc = acc;
+  bool fro_exact = !fast;     // a_fro holds the exact ||A||_F
+  auto exact_fro = [&]() {
+    RawBuf<ff::F> sq;  // squares on all threads, summed in order
+    if (!sq.alloc(nn)) return false;
+    par_rows(nn, threads, [&](size_t a, size_t b) {
+      for (size_t e = a; e < b; ++e) sq[e] = ff::fmul(Af[e], Af[e], pi);
     });
-    // one pass: fixed-width copy, its square and its k binary64 heads
-    // (bf_to_multicomp)
+    ff::F acc;
+    for (size_t e = 0; e < nn; ++e) acc = ff::fadd(acc, sq[e], pi);
+    a_fro = lf_sqrt(ff::to_bf(acc), p);
+    fro_exact = true;
+    return true;
+  };
+  if (fast) {
+    // one pass: fixed-width copy and its k binary64 heads (bf_to_multicomp)
     std::vector<char> bad(T, 0);
     std::vector<std::thread> ws;
     for (int t = 0; t < T; ++t)
@@ -426,22 +432,17 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
         for (size_t e = a; e < b; ++e) {
           const ff::F v = ff::from_bf(Avals[e], pi);
           Af[e] = v;
-          Sq[e] = ff::fmul(v, v, pi);
           if (!ff::to_multicomp(v, k, pi, c) &&
               bn::to_multicomp(Avals[e], k, c)) {
             bad[t] = 1;
             break;
           }
           for (int q = 0; q < k; ++q) a_pl[(size_t)q * nn + e] = c[q];
-          if ((e - a) % 512 == 511)
-            done[t].store(e - a + 1, std::memory_order_release);
         }
-        done[t].store(b - a, std::memory_order_release);
       });
     for (auto &w : ws) w.join();
     for (int t = 0; t < T; ++t)
       if (bad[t]) {
-        abort_sum.store(true);
         err = "value does not fit in binary64";
         return 5;
       }
@@ -455,8 +456,72 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
     for (const BF &s : sq) acc = lf_add(acc, s, p);
     a_fro = lf_sqrt(acc, p);
   }
+  // Rigorous bounds on ||A||_F from the binary64 heads (a_pl plane 0):
+  // check_stop's threshold is monotone in ||A||_F, so a comparison that
+  // falls outside [threshold(a_lo), threshold(a_hi)) is decided without the
+  // exact (sequentially rounded) sum, which keeps running on its thread
+  // and is waited for only when a comparison lands inside the bracket.
+  BF a_lo, a_hi;
+  bool have_bounds = false;
+  // MPCORE_REFINE_EXACT_FRO=1: always form the exact ||A||_F (tests)
+  const bool force_exact = std::getenv("MPCORE_REFINE_EXACT_FRO") != nullptr;
+  if (fast && !force_exact) {
+    // one chunk per thread, t-th chunk [nn t / T, nn (t + 1) / T)
+    auto par_chunks = [&](auto f) {
+      std::vector<std::thread> th;
+      for (int t = 0; t < T; ++t)
+        th.emplace_back([&, t] { f(t, nn * t / T, nn * (t + 1) / T); });
+      for (auto &x : th) x.join();
+    };
+    std::vector<int> emaxs(T, INT_MIN);
+    par_chunks([&](int t, size_t a, size_t b) {
+      int e = INT_MIN;
+      for (size_t q = a; q < b; ++q)
+        if (a_pl[q] != 0.0) e = std::max(e, std::ilogb(a_pl[q]));
+      emaxs[t] = e;
+    });
+    int emax = INT_MIN;
+    for (int e : emaxs) emax = std::max(emax, e);
+    const double eps = (double)(nn + 64) * 0x1p-52 + 0x1p-50;
+    if (emax != INT_MIN && eps < 0x1p-12) {
+      std::vector<double> part(T, 0.0);
+      par_chunks([&](int t, size_t a, size_t b) {
+        double acc = 0.0;
+        for (size_t q = a; q < b; ++q) {
+          const double v = std::ldexp(a_pl[q], -emax);
+          acc += v * v;
+        }
+        part[t] = acc;
+      });
+      double S = 0.0;
+      for (double v : part) S += v;
+      // heads: relative error 2^-53 each (squares 2^-52); sums of nn terms
+      // (nn + T) u; underflowed squares at most nn 2^-1022 in total
+      const double lo2 = S * (1.0 - eps) - (double)nn * 0x1p-1000;
+      const double hi2 = S * (1.0 + eps) + (double)nn * 0x1p-1000;
+      const double lo = lo2 > 0.0 ? std::sqrt(lo2) * (1.0 - 0x1p-40) : 0.0;
+      const double hi = std::sqrt(hi2) * (1.0 + 0x1p-40);
+      if (std::isfinite(hi)) {
+        a_lo = bn::from_binary64(lo);
+        a_hi = bn::from_binary64(hi);
+        if (a_lo.sign) a_lo.exp += emax;
+        a_hi.exp += emax;
+        have_bounds = true;
+      }
+    }
+  }
   plog.mark("A -> fixed, planes");
   if ((st = to_planes(Bvals, k, b_pl.data(), (size_t)n, err))) return st;
+  std::vector<ff::F> Bf;
+  bool use_dev = false;
+  if (fast) {
+    Bf.resize(n);
+    for (int i = 0; i < n; ++i) Bf[i] = ff::from_bf(Bvals[i], pi);
+    if (dev_res) {  // upload (asynchronous) overlaps the factorisation
+      if ((st = S.residual_setup(n, pi, Af.p, Bf.data(), err))) return st;
+      use_dev = true;
+    }
+  }
   const auto t1 = Clock::now();
   if ((st = S.factor(k, n, a_pl.p, err))) return st;
   const auto t2 = Clock::now();
@@ -507,16 +572,15 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
     }
   };
   std::vector<BF> x;
-  std::vector<ff::F> xf, resf, zf, Bf;
+  std::vector<ff::F> xf, resf, zf;
   if (fast) {
     lift_f(x_pl, xf);
-    Bf.resize(n);
-    for (int i = 0; i < n; ++i) Bf[i] = ff::from_bf(Bvals[i], pi);
   } else {
     lift(x_pl, x);
   }
   plog.mark("lift x");
   const BF one = from_int(1, p);
+  const BF sqrt_n = lf_sqrt(from_int(n, p), p);
   std::vector<BF> res(n), work(n), z;
   auto norm2_f = [&](const std::vector<ff::F> &v) {
     ff::F acc;
@@ -530,7 +594,13 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
     // res = b - A x  (scalar mat_vec order per row, linalg.py:566-574)
     const auto ta = Clock::now();
     BF res_norm, x_norm;
-    if (fast) {
+    if (use_dev) {
+      resf.resize(n);
+      if ((st = S.residual(xf.data(), resf.data(), err))) return st;
+      t_res += secs(ta, Clock::now());
+      res_norm = norm2_f(resf);
+      x_norm = norm2_f(xf);
+    } else if (fast) {
       resf.resize(n);
       par_rows((size_t)n, threads, [&](size_t r0, size_t r1) {
         for (size_t i = r0; i < r1; ++i) {
@@ -544,11 +614,6 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
       t_res += secs(ta, Clock::now());
       res_norm = norm2_f(resf);
       x_norm = norm2_f(xf);
-      if (fro.joinable()) {
-        fro.join();
-        a_fro = lf_sqrt(ff::to_bf(fro_acc), p);
-        plog.mark("||A||_F (join)");
-      }
     } else {
       par_rows((size_t)n, threads, [&](size_t r0, size_t r1) {
         for (size_t i = r0; i < r1; ++i) {
@@ -566,12 +631,31 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
     plog.mark("residual + norms");
     out.residuals.push_back(res_norm);
     if (res_norm.sign == 0) { reason = "converged"; break; }
-    BF t = lf_sqrt(from_int(n, p), p);
-    t = lf_mul(t, rtol, p);
-    t = lf_mul(t, a_fro, p);
-    t = lf_mul(t, x_norm, p);
-    t = lf_add(t, atol, p);
-    if (lf_cmp(res_norm, t) < 0) { reason = "converged"; break; }
+    // check_stop (refine.py:104-118): res < sqrt(n) rtol ||A||_F ||x|| + atol
+    auto threshold = [&](const BF &af) {
+      BF t = sqrt_n;
+      t = lf_mul(t, rtol, p);
+      t = lf_mul(t, af, p);
+      t = lf_mul(t, x_norm, p);
+      return lf_add(t, atol, p);
+    };
+    bool conv;
+    if (!fro_exact && have_bounds && lf_cmp(res_norm, threshold(a_lo)) < 0) {
+      conv = true;
+    } else if (!fro_exact && have_bounds &&
+               lf_cmp(res_norm, threshold(a_hi)) >= 0) {
+      conv = false;
+    } else {
+      if (!fro_exact) {
+        if (!exact_fro()) {
+          err = "out of host memory";
+          return 6;
+        }
+        plog.mark("||A||_F (exact)");
+      }
+      conv = lf_cmp(res_norm, threshold(a_fro)) < 0;
+    }
+    if (conv) { reason = "converged"; break; }
     const size_t h = out.residuals.size();
     if (h >= 4 && lf_cmp(out.residuals[h - 1], out.residuals[h - 2]) >= 0 &&
         lf_cmp(out.residuals[h - 2], out.residuals[h - 3]) >= 0 &&
@@ -610,9 +694,6 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
     }
     ++corrections;
     plog.mark("correction");
-  }
-  if (fro.joinable()) {  // (stopped before the first check)
-    fro.join();
   }
   if (fast) {
     x.resize(n);
@@ -710,6 +791,78 @@ int64_t longfloat_selftest(int64_t iters, uint64_t seed, int p) {
       }
     }
   }
+  return bad;
+}
+
+// The device long residual (residual.cu) against the host's fixed-width
+// one on a random n x n system at precision p: rows whose residual differs
+// in any bit (sign, exponent or mantissa limb).  -1: bad arguments / CUDA.
+int64_t long_residual_selftest(int n, int p, uint64_t seed, cudaStream_t s) {
+  if (n <= 0 || p < 2 || p > 512) return -1;
+  uint64_t z = seed;
+  auto rnd = [&]() {
+    z += 0x9E3779B97F4A7C15ull;
+    uint64_t x = z;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+  };
+  const int nl = (p + 63) >> 6;
+  auto rand_f = [&](int64_t ec) {
+    ff::F v;
+    v.sign = (rnd() & 1) ? 1 : -1;
+    for (int i = 0; i < ff::NL; ++i) v.m[i] = i < nl ? rnd() : 0;
+    if (rnd() % 8 == 0)  // runs of ones: carries through every limb
+      for (int i = 0; i < nl; ++i) v.m[i] = ~0ull;
+    for (int b = p; b < 64 * nl; ++b) v.m[b >> 6] &= ~(1ull << (b & 63));
+    v.m[(p - 1) >> 6] |= 1ull << ((p - 1) & 63);
+    v.exp = ec - p;
+    if (rnd() % 64 == 0) v = ff::F();  // zeros
+    return v;
+  };
+  const size_t nn = (size_t)n * n;
+  std::vector<ff::F> A(nn), x(n), b(n), r_host(n), r_dev(n);
+  for (auto &v : A) v = rand_f((int64_t)(rnd() % 40) - 20);
+  for (auto &v : x) v = rand_f((int64_t)(rnd() % 40) - 20);
+  // b close to A x in some rows (cancellation), random elsewhere
+  for (int i = 0; i < n; ++i) {
+    ff::F acc;
+    for (int j = 0; j < n; ++j)
+      acc = ff::fadd(acc, ff::fmul(A[(size_t)i * n + j], x[j], p), p);
+    if (i % 3 == 0) {
+      b[i] = acc;
+      if (i % 6 == 0 && acc.sign != 0) b[i].m[0] ^= 1ull << ((nl * 64 - p) & 63);
+    } else {
+      b[i] = rand_f((int64_t)(rnd() % 40) - 10);
+    }
+    r_host[i] = ff::fadd(b[i], ff::neg(acc), p);
+  }
+  void *dA = nullptr, *dx = nullptr, *db = nullptr, *dr = nullptr;
+  const size_t fb = sizeof(ff::F);
+  int64_t bad = -1;
+  if (cudaMalloc(&dA, nn * fb) == cudaSuccess &&
+      cudaMalloc(&dx, n * fb) == cudaSuccess &&
+      cudaMalloc(&db, n * fb) == cudaSuccess &&
+      cudaMalloc(&dr, n * fb) == cudaSuccess &&
+      cudaMemcpy(dA, A.data(), nn * fb, cudaMemcpyHostToDevice) == cudaSuccess &&
+      cudaMemcpy(dx, x.data(), n * fb, cudaMemcpyHostToDevice) == cudaSuccess &&
+      cudaMemcpy(db, b.data(), n * fb, cudaMemcpyHostToDevice) == cudaSuccess &&
+      mpk::long_residual(p, n, dA, dx, db, dr, s) == cudaSuccess &&
+      cudaStreamSynchronize(s) == cudaSuccess &&
+      cudaMemcpy(r_dev.data(), dr, n * fb, cudaMemcpyDeviceToHost) == cudaSuccess) {
+    bad = 0;
+    for (int i = 0; i < n; ++i) {
+      const ff::F &u = r_host[i], &v = r_dev[i];
+      bool same = u.sign == v.sign;
+      if (same && u.sign != 0) {
+        same = u.exp == v.exp;
+        for (int l = 0; l < nl; ++l) same = same && u.m[l] == v.m[l];
+      }
+      if (!same) ++bad;
+    }
+  }
+  for (void *q : {dA, dx, db, dr})
+    if (q) cudaFree(q);
   return bad;
 }
 

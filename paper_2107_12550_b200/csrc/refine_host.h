@@ -5,6 +5,7 @@
 // short-precision factor/solve on the GPU through ShortSolver.
 #pragma once
 #include <cstdint>
+#include <cuda_runtime.h>
 #include <string>
 #include <vector>
 
@@ -33,6 +34,17 @@ class ShortSolver {
                      std::string &err) = 0;
   virtual int solve(const std::vector<double> &b_planes,
                     std::vector<double> &x_planes, std::string &err) = 0;
+  // Optional: the long residual b - A x on the device.
+  // Values travel as fixed-width long floats (fastfloat.h ff::F, p <= 512).
+  virtual bool residual_supported(int p) { return false; }
+  // a host buffer of `bytes` the solver keeps (page-locked, reused across
+  // calls) for the fixed-width A, or null
+  virtual void *staging(size_t bytes) { return nullptr; }
+  // A (n x n, row-major, in staging memory) and b; the upload may proceed
+  // asynchronously, overlapping the factorisation
+  virtual int residual_setup(int n, int p, const void *A, const void *b,
+                             std::string &err) { return 6; }
+  virtual int residual(const void *x, void *res, std::string &err) { return 6; }
 };
 
 // -> status (0 ok, 2 dims, 3 singular, 4 parse/file, 5 overflow, 6 other)
@@ -51,6 +63,10 @@ int refine_core(std::vector<bn::BF> &A, std::vector<bn::BF> &B, int n,
 // fastfloat.h against the generic big-integer path: mismatches over iters
 // random operand pairs at precision p (-1: p out of the fixed-width range)
 int64_t longfloat_selftest(int64_t iters, uint64_t seed, int p);
+
+// the device long residual (residual.cu) against the host's on a random
+// n x n system at precision p <= 512: mismatching rows, -1 on error
+int64_t long_residual_selftest(int n, int p, uint64_t seed, cudaStream_t s);
 
 // bf_format_hex (bigfloat.py:524-537) and a .mpmat writer (matfile.py
 // layout: header "mpmat rows cols bf bits", one row per line)

@@ -132,10 +132,17 @@ def write_bf(path, rows_hex, bits):
             fh.write(" ".join(row) + "\n")
 
 
+@pytest.mark.parametrize("exact_fro", [False, True])
 @pytest.mark.parametrize("idx", range(5))
-def test_native_refine_matches_reference(tmp_path, idx):
+def test_native_refine_matches_reference(tmp_path, idx, exact_fro,
+                                         monkeypatch):
     """mpcore_refine (ffi.py:243-258): native long arithmetic + GPU short
-    solves reproduce the reference's IR run bit for bit."""
+    solves (and the GPU long residual) reproduce the reference's IR run bit
+    for bit -- with check_stop decided from the rigorous ||A||_F bounds
+    where they suffice (default) and with the exact ||A||_F always formed
+    (MPCORE_REFINE_EXACT_FRO)."""
+    if exact_fro:
+        monkeypatch.setenv("MPCORE_REFINE_EXACT_FRO", "1")
     case = G["refine"][idx]
     p = case["long_bits"]
     a_path, b_path = str(tmp_path / "A.mpmat"), str(tmp_path / "b.mpmat")

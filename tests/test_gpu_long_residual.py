@@ -1,0 +1,29 @@
+"""The IR residual b - A x at long precision on the GPU (SURVEY §8(f) row 1,
+csrc/residual.cu) against the host's fixed-width arithmetic (itself checked
+against the generic big-integer path, test_longside.py) on random systems
+with cancellation rows, zeros and all-ones mantissas: bit for bit.  The
+golden IR runs (test_gpu_config3.py, test_gpu_ffi.py) go through it too."""
+
+import ctypes
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("prec", [53, 64, 65, 106, 200, 300, 424, 511, 512])
+@pytest.mark.parametrize("n", [1, 7, 33])
+def test_device_residual_matches_host(prec, n):
+    from paper_2107_12550_b200 import _native as nat
+    m = ctypes.c_int64(-1)
+    nat.check(nat.lib().mpcore_debug_long_residual_selftest(
+        n, prec, 2107 + prec * 31 + n, ctypes.byref(m)), "residual selftest")
+    assert m.value == 0
+
+
+def test_device_residual_larger():
+    from paper_2107_12550_b200 import _native as nat
+    m = ctypes.c_int64(-1)
+    nat.check(nat.lib().mpcore_debug_long_residual_selftest(
+        256, 512, 99, ctypes.byref(m)), "residual selftest")
+    assert m.value == 0
