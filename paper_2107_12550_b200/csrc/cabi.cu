@@ -608,8 +608,8 @@ struct IrWorkspace {
   size_t acap = 0, bcap = 0, xcap = 0, pcap = 0;
   // the long residual (residual.cu): page-locked staging of the
   // fixed-width A, its device copy, vectors, and the upload stream
-  void *stage = nullptr, *hx = nullptr, *hres = nullptr;
-  size_t stagecap = 0, hcap = 0;
+  void *stage = nullptr, *hx = nullptr, *hres = nullptr, *stage_pl = nullptr;
+  size_t stagecap = 0, hcap = 0, stage_plcap = 0;
   void *rA = nullptr, *rb = nullptr, *rx = nullptr, *rres = nullptr;
   size_t rAcap = 0, rbcap = 0, rxcap = 0, rrcap = 0;
   cudaStream_t up = nullptr;
@@ -719,13 +719,15 @@ class GpuShortSolver : public mpr::ShortSolver {
   }
   // ---- the long residual on the device (residual.cu) ----
   bool residual_supported(int p) override { return p <= 512 && claim(); }
-  void *staging(size_t bytes) override {
-    if (!claim()) return nullptr;
+  void *staging(int slot, size_t bytes) override {
+    if (!claim() || slot < 0 || slot > 1) return nullptr;
     DevLock L;
     if (L.st) return nullptr;
     IrWorkspace &w = ir_ws();
-    if (grow_host(&w.stage, w.stagecap, bytes) != cudaSuccess) return nullptr;
-    return w.stage;
+    void **p = slot == 0 ? &w.stage : &w.stage_pl;
+    size_t &cap = slot == 0 ? w.stagecap : w.stage_plcap;
+    if (grow_host(p, cap, bytes) != cudaSuccess) return nullptr;
+    return *p;
   }
   int residual_setup(int n, int p, const void *A, const void *b,
                      std::string &err) override {

@@ -392,10 +392,16 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
   // fixed-width A is then written straight into its page-locked staging
   const bool dev_res = fast && S.residual_supported(pi);
   if (dev_res) {
-    if (void *st_buf = S.staging(nn * sizeof(ff::F)))
+    if (void *st_buf = S.staging(0, nn * sizeof(ff::F)))
       Af.adopt(static_cast<ff::F *>(st_buf));
   }
-  if (!a_pl.alloc((size_t)k * nn) ||
+  // the short planes too (the factorisation's upload from page-locked
+  // memory runs at the link's rate)
+  if (fast && S.residual_supported(pi)) {
+    if (void *st_buf = S.staging(1, (size_t)k * nn * sizeof(double)))
+      a_pl.adopt(static_cast<double *>(st_buf));
+  }
+  if ((a_pl.p == nullptr && !a_pl.alloc((size_t)k * nn)) ||
       (fast && Af.p == nullptr && !Af.alloc(nn))) {
     err = "out of host memory";
     return 6;

@@ -38,8 +38,8 @@ class ShortSolver {
   // Values travel as fixed-width long floats (fastfloat.h ff::F, p <= 512).
   virtual bool residual_supported(int p) { return false; }
   // a host buffer of `bytes` the solver keeps (page-locked, reused across
-  // calls) for the fixed-width A, or null
-  virtual void *staging(size_t bytes) { return nullptr; }
+  // calls), or null: slot 0 the fixed-width A, slot 1 the short planes
+  virtual void *staging(int slot, size_t bytes) { return nullptr; }
   // A (n x n, row-major, in staging memory) and b; the upload may proceed
   // asynchronously, overlapping the factorisation
   virtual int residual_setup(int n, int p, const void *A, const void *b,
