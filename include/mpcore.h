@@ -261,10 +261,11 @@ int32_t mpcore_debug_solve_trace(uint64_t *out_ns, int64_t cap);
  * the generic big-integer path on random operands at precision prec
  * (<= 640); host only */
 /* Diagnostics: the device long residual b - A x
-   against the host's on a random n x n system at precision prec <= 512;
+   against the host's on a random n x n system at precision prec <= 512
+   (variant 0: warp per row, the production kernel; 1: thread per row);
    mismatching rows in *mismatches.  Extension. */
 int32_t mpcore_debug_long_residual_selftest(int32_t n, int32_t prec,
-                                            uint64_t seed,
+                                            uint64_t seed, int32_t variant,
                                             int64_t *mismatches);
 int32_t mpcore_debug_longfloat_selftest(int64_t iters, uint64_t seed,
                                         int32_t prec, int64_t *mismatches);

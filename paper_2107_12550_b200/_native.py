@@ -73,7 +73,7 @@ _PROTOS = {
     "mpcore_debug_panel_trace": (_i32, [ctypes.POINTER(_u64), _i64]),
     "mpcore_debug_lu_stamps": (_i32, [_i64, ctypes.POINTER(_u64)]),
     "mpcore_stream_event_record": (_i32, [_i32]),
-    "mpcore_debug_long_residual_selftest": (_i32, [_i32, _i32, _u64, ctypes.POINTER(_i64)]),
+    "mpcore_debug_long_residual_selftest": (_i32, [_i32, _i32, _u64, _i32, ctypes.POINTER(_i64)]),
     "mpcore_stream_event_elapsed": (_i32, [_i32, _i32, ctypes.POINTER(ctypes.c_double)]),
     "mpcore_solve_system": (_i32, [_u64, _u64, _u64, _i32, ctypes.POINTER(_u64),
                                    ctypes.POINTER(_i32)]),

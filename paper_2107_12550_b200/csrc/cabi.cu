@@ -1414,12 +1414,13 @@ int32_t mpcore_debug_panel_trace(uint64_t *out_ns, int64_t cap) {
 }
 
 int32_t mpcore_debug_long_residual_selftest(int32_t n, int32_t prec,
-                                            uint64_t seed,
+                                            uint64_t seed, int32_t variant,
                                             int64_t *mismatches) {
-  if (!mismatches) return MPCORE_BAD_DIMENSION;
+  if (!mismatches || variant < 0 || variant > 1) return MPCORE_BAD_DIMENSION;
   DevLock L;
   if (L.st) return L.st;
-  *mismatches = mpr::long_residual_selftest(n, prec, seed, device().stream);
+  *mismatches = mpr::long_residual_selftest(n, prec, seed, device().stream,
+                                            variant);
   return *mismatches < 0 ? MPCORE_INTERNAL : MPCORE_OK;
 }
 

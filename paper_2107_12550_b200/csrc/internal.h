@@ -52,9 +52,11 @@ struct LuWork {
 int num_sms();
 // IR residual b - A x at long precision p <= 512 on the device (residual.cu):
 // A row-major n x n, x, b, res length n, all as fixed-width long floats
-// (longfloat.cuh lf::DF = the host's ff::F)
+// (longfloat.cuh lf::DF = the host's ff::F); variant 0: a warp per row
+// (longwarp.cuh, the production path), 1: a thread per row (longfloat.cuh)
 cudaError_t long_residual(int p, int n, const void *A, const void *x,
-                          const void *b, void *res, cudaStream_t s);
+                          const void *b, void *res, cudaStream_t s,
+                          int variant = 0);
 // diagnostics: per-panel kernel stamps into buf ([4 * n] u64) or off (null)
 cudaError_t lu_stamps_enable(unsigned long long *buf);
 

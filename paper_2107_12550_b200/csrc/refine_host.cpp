@@ -489,7 +489,9 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
     int emax = INT_MIN;
     for (int e : emaxs) emax = std::max(emax, e);
     const double eps = (double)(nn + 64) * 0x1p-52 + 0x1p-50;
-    if (emax != INT_MIN && eps < 0x1p-12) {
+    // (heads far from the subnormal range: each within 2^-53 of its value,
+    // and subnormal heads of tiny elements negligible against the slack)
+    if (emax != INT_MIN && emax > -900 && eps < 0x1p-12) {
       std::vector<double> part(T, 0.0);
       par_chunks([&](int t, size_t a, size_t b) {
         double acc = 0.0;
@@ -803,7 +805,8 @@ int64_t longfloat_selftest(int64_t iters, uint64_t seed, int p) {
 // The device long residual (residual.cu) against the host's fixed-width
 // one on a random n x n system at precision p: rows whose residual differs
 // in any bit (sign, exponent or mantissa limb).  -1: bad arguments / CUDA.
-int64_t long_residual_selftest(int n, int p, uint64_t seed, cudaStream_t s) {
+int64_t long_residual_selftest(int n, int p, uint64_t seed, cudaStream_t s,
+                               int variant) {
   if (n <= 0 || p < 2 || p > 512) return -1;
   uint64_t z = seed;
   auto rnd = [&]() {
@@ -853,7 +856,7 @@ int64_t long_residual_selftest(int n, int p, uint64_t seed, cudaStream_t s) {
       cudaMemcpy(dA, A.data(), nn * fb, cudaMemcpyHostToDevice) == cudaSuccess &&
       cudaMemcpy(dx, x.data(), n * fb, cudaMemcpyHostToDevice) == cudaSuccess &&
       cudaMemcpy(db, b.data(), n * fb, cudaMemcpyHostToDevice) == cudaSuccess &&
-      mpk::long_residual(p, n, dA, dx, db, dr, s) == cudaSuccess &&
+      mpk::long_residual(p, n, dA, dx, db, dr, s, variant) == cudaSuccess &&
       cudaStreamSynchronize(s) == cudaSuccess &&
       cudaMemcpy(r_dev.data(), dr, n * fb, cudaMemcpyDeviceToHost) == cudaSuccess) {
     bad = 0;

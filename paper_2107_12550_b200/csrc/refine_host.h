@@ -65,8 +65,10 @@ int refine_core(std::vector<bn::BF> &A, std::vector<bn::BF> &B, int n,
 int64_t longfloat_selftest(int64_t iters, uint64_t seed, int p);
 
 // the device long residual (residual.cu) against the host's on a random
-// n x n system at precision p <= 512: mismatching rows, -1 on error
-int64_t long_residual_selftest(int n, int p, uint64_t seed, cudaStream_t s);
+// n x n system at precision p <= 512 (variant: see mpk::long_residual):
+// mismatching rows, -1 on error
+int64_t long_residual_selftest(int n, int p, uint64_t seed, cudaStream_t s,
+                               int variant);
 
 // bf_format_hex (bigfloat.py:524-537) and a .mpmat writer (matfile.py
 // layout: header "mpmat rows cols bf bits", one row per line)

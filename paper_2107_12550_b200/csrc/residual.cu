@@ -10,8 +10,6 @@
 #include "longfloat.cuh"
 #include "longwarp.cuh"
 
-#include <cstdlib>
-
 namespace mpk {
 
 namespace {
@@ -73,10 +71,10 @@ long_residual_warp_kernel(const lf::DF *__restrict__ A,
 }  // namespace
 
 cudaError_t long_residual(int p, int n, const void *A, const void *x,
-                          const void *b, void *res, cudaStream_t s) {
+                          const void *b, void *res, cudaStream_t s,
+                          int variant) {
   if (n <= 0) return cudaSuccess;
-  static const bool per_thread = std::getenv("MPCORE_RESIDUAL_THREAD") != nullptr;
-  if (!per_thread && p <= 512) {
+  if (variant == 0 && p <= 512) {
     long_residual_warp_kernel<<<(n + 3) / 4, 128, 0, s>>>(
         static_cast<const lf::DF *>(A), static_cast<const lf::DF *>(x),
         static_cast<const lf::DF *>(b), static_cast<lf::DF *>(res), n, p);
