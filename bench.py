@@ -172,8 +172,14 @@ def cpu_baseline(k, n_sample, threads=None):
     path) on a bounded sample: LU + solve of the same recipe at n_sample."""
     import oracle
     from oracle import gen
-    if threads:
-        oracle.set_threads(threads)
+    # every host thread this process may run on (torchrun sets
+    # OMP_NUM_THREADS=1 per rank; the baseline runs on rank 0 alone)
+    if not threads:
+        try:
+            threads = len(os.sched_getaffinity(0))
+        except AttributeError:
+            threads = os.cpu_count() or 1
+    oracle.set_threads(threads)
     cores = oracle.num_threads()
     A = gen.planes(k, (n_sample, n_sample), 0, n_sample, SEED)
     x = gen.planes(k, (n_sample,), 2, n_sample, SEED)
