@@ -413,6 +413,80 @@ def traffic_bytes(k, n):
     return d["dram_bytes"] if (d.get("k"), d.get("n")) == (k, n) else None
 
 
+def run_single_config4(args):
+    """BASELINE config 4 at one GPU: the same seeded system (one rank's
+    column-block-cyclic layout is the plain layout) through the one-call
+    LU + solve ([A | b] factored together, back substitution); bitwise the
+    distributed protocol's result (tests/test_gpu_dist.py)."""
+    from paper_2107_12550_b200 import _native as nat
+    from paper_2107_12550_b200.linalg import DeviceMatrix, DeviceVector
+    k, n = args.k, args.n
+    seed = 210712550 + 4
+    L = nat.lib()
+    A0 = DeviceMatrix(k, n, n)
+    A0.generate(0, n, seed)
+    ones = np.zeros((k, n))
+    ones[0] = 1.0
+    xt = DeviceVector.from_planes(ones)
+    b = DeviceVector(k, n)
+    nat.check(L.mpcore_mat_vec(A0.handle, xt.handle, b.handle), "mat_vec")
+    W = DeviceMatrix(k, n, n + 1)
+    x = DeviceVector(k, n)
+    a0p, bp, wp, xp = (A0.device_ptr(), b.device_ptr(), W.device_ptr(),
+                       x.device_ptr())
+    sw = np.zeros(n, dtype=np.int32)
+    sstep = ctypes.c_int32()
+
+    def step():
+        nat.check(L.mpcore_dev_copy2d(k, n, n, wp, n + 1, n * (n + 1), a0p, n,
+                                      n * n), "restore A")
+        nat.check(L.mpcore_dev_copy2d(k, n, 1, wp + n * 8, n + 1, n * (n + 1),
+                                      bp, 1, n), "restore b")
+        nat.check(L.mpcore_dev_solve_system(
+            k, n, wp, n + 1, n * (n + 1), 0, xp,
+            sw.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+            ctypes.byref(sstep)), "solve_system")
+
+    for _ in range(args.warmup):
+        step()
+    nat.sync()
+    timer = nat.StreamTimer()
+    with ClockSampler(0) as clk:
+        timer.start()
+        for _ in range(args.steps):
+            step()
+        ms = timer.stop() / args.steps
+        nat.sync()
+    xs = x.download()
+    err = float(np.max(np.abs((xs[0] - 1.0) + xs[1])))
+    flops = (2.0 / 3.0) * n ** 3
+    wc = work_counts(n, k)
+    line = {
+        "metric": "%s LU+solve eff. GFLOP/s ((2/3)n^3/s)" % NAMES[k],
+        "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64x%d (%s, bit-exact EFT arithmetic)" % (k, NAMES[k]),
+        "data": "synthetic (seeded recipe, SURVEY 8d; seed %d)" % seed,
+        "config": {"workload": "config4: distributed %s LU+PP+solve n=%d"
+                   % (NAMES[k], n), "n": n, "k": k, "nb": 32,
+                   "parallelism": "one GPU: the one-rank column-block-cyclic "
+                   "layout is the plain layout; one-call LU + solve "
+                   "(--dist-protocol runs the distributed driver instead)",
+                   "l2": "A restored from a pristine copy each step (>> L2)"},
+        "check": {"max_abs_err_x_vs_ones": err},
+        "roofline": {"bound": "fp64",
+                     "achieved": wc["instr"] / (ms * 1e-3) / 1e12,
+                     "unit": "T FP64 instr/s", "peak": 18.2,
+                     "frac": wc["instr"] / (ms * 1e-3) / 18.2e12,
+                     "traffic": None},
+        "e2e": None, "gpu_launches": None,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+
+
 def run_dist(args):
     """BASELINE config 4: distributed DD LU (+ solve) of one n x n system,
     column-block-cyclic over the ranks (nb = 256), NCCL panel + pivot
@@ -726,6 +800,8 @@ def main():
     ap.add_argument("--cpu-n", type=int, default=0,
                     help="CPU baseline sample size (0: the workload n)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist-protocol", action="store_true",
+                    help="config 4 at one GPU through the distributed driver")
     args = ap.parse_args()
     if args.config == 4:
         args.k = args.k or 2
@@ -742,7 +818,11 @@ def main():
     if args.impl == "reference":
         run_reference(args)
     elif args.config == 4:
-        run_dist(args)
+        if int(os.environ.get("WORLD_SIZE", "1")) == 1 and \
+                not args.dist_protocol:
+            run_single_config4(args)
+        else:
+            run_dist(args)
     elif args.config == 3:
         run_config3(args)
     elif args.config == 1:
