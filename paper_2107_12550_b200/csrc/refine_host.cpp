@@ -373,15 +373,18 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
   if (rtol.sign == 0 && atol.sign == 0) { err = "rtol and atol cannot both be zero"; return 6; }
   const auto t0 = Clock::now();
   PhaseLog plog;
-  // re-round into the working context (convert_* BfDomain -> BfDomain)
-  par_rows(Avals.size(), threads, [&](size_t a, size_t b) {
-    for (size_t e = a; e < b; ++e) Avals[e] = lf_round(Avals[e], p);
-  });
-  for (auto &v : Bvals) v = lf_round(v, p);
-  plog.mark("round A, b");
   // short copies; transfer precision max(long, 53k+64)+8 (linalg.py:743)
   const int64_t p_in = std::max<int64_t>(p, 53 * k + 64) + 8;
   const bool fast = p_in <= 64 * ff::NL;   // fixed-width path (fastfloat.h)
+  // re-round into the working context (convert_* BfDomain -> BfDomain);
+  // the fixed-width path rounds A once in its conversion pass (from_bf)
+  if (!fast) {
+    par_rows(Avals.size(), threads, [&](size_t a, size_t b) {
+      for (size_t e = a; e < b; ++e) Avals[e] = lf_round(Avals[e], p);
+    });
+  }
+  for (auto &v : Bvals) v = lf_round(v, p);
+  plog.mark("round A, b");
   const int pi = (int)p;
   const size_t nn = (size_t)n * n;
   // n x n buffers are first touched by the threads that fill them (a
@@ -439,7 +442,7 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
           const ff::F v = ff::from_bf(Avals[e], pi);
           Af[e] = v;
           if (!ff::to_multicomp(v, k, pi, c) &&
-              bn::to_multicomp(Avals[e], k, c)) {
+              bn::to_multicomp(ff::to_bf(v), k, c)) {
             bad[t] = 1;
             break;
           }
