@@ -536,8 +536,13 @@ cudaError_t enqueue_lu(int k, int m, int ncols, MatView A, int32_t *d_swaps,
       const char *e = std::getenv("MPCORE_NEXT_MAIN_COLS");
       return e ? std::atoi(e) : 700;
     }();
+    static const int nm_cols_dd = [] {
+      const char *e = std::getenv("MPCORE_NEXT_MAIN_COLS_DD");
+      return e ? std::atoi(e) : INT_MAX;
+    }();
     const bool next_on_main =
-        nm_env ? std::atoi(nm_env) != 0 : (k == 2 || rest_c - w2 < nm_cols);
+        nm_env ? std::atoi(nm_env) != 0
+               : rest_c - w2 < (k == 2 ? nm_cols_dd : nm_cols);
     cudaStream_t ns = next_on_main ? s : ws.side;
     if (next_on_main &&
         (e = lu_update(k, rest_r, w2, w, sub(A, J2, J), sub(A, J, J2),
