@@ -153,27 +153,75 @@ UBig UBig::mul(const UBig &a, const UBig &b) {
   return r;
 }
 
+// Schoolbook long division on 32-bit limbs (Knuth's Algorithm D: normalise
+// the divisor's top bit, estimate each quotient limb from the top two limbs
+// and correct at most twice, multiply-subtract, add back on a borrow).
 void UBig::divmod(const UBig &a, const UBig &b, UBig &q, UBig &r) {
   q = UBig();
   r = UBig();
-  if (cmp(a, b) < 0) {
+  if (b.zero() || cmp(a, b) < 0) {  // (division by zero: callers exclude it)
     r = a;
     return;
   }
-  int64_t nb = a.bits();
-  q.w.assign((size_t)((nb + 31) / 32), 0u);
-  for (int64_t i = nb - 1; i >= 0; --i) {
-    r = r.shl(1);
-    if (a.bit(i)) {
-      if (r.w.empty()) r.w.push_back(1u);
-      else r.w[0] |= 1u;
+  const size_t n = b.w.size(), na = a.w.size();
+  if (n == 1) {
+    const uint64_t d = b.w[0];
+    uint64_t rem = 0;
+    q.w.assign(na, 0u);
+    for (size_t i = na; i-- > 0;) {
+      const uint64_t cur = (rem << 32) | a.w[i];
+      q.w[i] = (uint32_t)(cur / d);
+      rem = cur % d;
     }
-    if (cmp(r, b) >= 0) {
-      r = sub(r, b);
-      q.w[(size_t)(i / 32)] |= 1u << (i % 32);
-    }
+    q.trim();
+    r = UBig(rem);
+    return;
   }
+  const int s = __builtin_clz(b.w[n - 1]);
+  std::vector<uint32_t> vn(n), un(na + 1);
+  for (size_t i = n - 1; i > 0; --i)
+    vn[i] = (b.w[i] << s) | (s ? (uint32_t)((uint64_t)b.w[i - 1] >> (32 - s)) : 0u);
+  vn[0] = b.w[0] << s;
+  un[na] = s ? (uint32_t)((uint64_t)a.w[na - 1] >> (32 - s)) : 0u;
+  for (size_t i = na - 1; i > 0; --i)
+    un[i] = (a.w[i] << s) | (s ? (uint32_t)((uint64_t)a.w[i - 1] >> (32 - s)) : 0u);
+  un[0] = a.w[0] << s;
+  const uint64_t B = 1ull << 32;
+  q.w.assign(na - n + 1, 0u);
+  for (size_t j = na - n + 1; j-- > 0;) {
+    const uint64_t num = ((uint64_t)un[j + n] << 32) | un[j + n - 1];
+    uint64_t qhat = num / vn[n - 1], rhat = num % vn[n - 1];
+    while (qhat >= B || qhat * vn[n - 2] > ((rhat << 32) | un[j + n - 2])) {
+      --qhat;
+      rhat += vn[n - 1];
+      if (rhat >= B) break;
+    }
+    int64_t k = 0, t;
+    for (size_t i = 0; i < n; ++i) {
+      const uint64_t p = qhat * vn[i];
+      t = (int64_t)un[i + j] - k - (int64_t)(p & 0xffffffffull);
+      un[i + j] = (uint32_t)t;
+      k = (int64_t)(p >> 32) - (t >> 32);
+    }
+    t = (int64_t)un[j + n] - k;
+    un[j + n] = (uint32_t)t;
+    if (t < 0) {  // qhat one too large: add the divisor back
+      --qhat;
+      uint64_t c = 0;
+      for (size_t i = 0; i < n; ++i) {
+        const uint64_t s2 = (uint64_t)un[i + j] + vn[i] + c;
+        un[i + j] = (uint32_t)s2;
+        c = s2 >> 32;
+      }
+      un[j + n] += (uint32_t)c;
+    }
+    q.w[j] = (uint32_t)qhat;
+  }
+  r.w.assign(n, 0u);
+  for (size_t i = 0; i < n; ++i)
+    r.w[i] = (un[i] >> s) | (s ? (uint32_t)((uint64_t)un[i + 1] << (32 - s)) : 0u);
   q.trim();
+  r.trim();
 }
 
 UBig UBig::isqrt(const UBig &a) {

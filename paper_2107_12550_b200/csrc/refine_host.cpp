@@ -768,6 +768,15 @@ int64_t longfloat_selftest(int64_t iters, uint64_t seed, int p) {
     if (lf_cmp(s, s_ref) != 0 || s.sign != s_ref.sign) ++bad;
     if (lf_cmp(d, d_ref) != 0 || d.sign != d_ref.sign) ++bad;
     if (lf_cmp(mm, m_ref) != 0 || mm.sign != m_ref.sign) ++bad;
+    // big-integer division (Knuth D): q b + r == a, r < b
+    if (!b.man.zero()) {
+      bn::UBig q, r;
+      const bn::UBig num = bn::UBig::mul(a.man, a.man.shl(rnd() % 70));
+      bn::UBig::divmod(num, b.man, q, r);
+      if (bn::UBig::cmp(bn::UBig::add(bn::UBig::mul(q, b.man), r), num) != 0 ||
+          bn::UBig::cmp(r, b.man) >= 0)
+        ++bad;
+    }
     // the compile-time-width kernels (fadd / fmul) on the same operands
     const BF s2 = ff::to_bf(ff::fadd(fa, fb, p));
     const BF d2 = ff::to_bf(ff::fadd(fa, ff::neg(fb), p));
