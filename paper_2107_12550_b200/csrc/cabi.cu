@@ -691,7 +691,8 @@ class GpuShortSolver : public mpr::ShortSolver {
       return MPCORE_INTERNAL;
     }
     if ((e = cudaMemcpy(a_, a, mb, cudaMemcpyHostToDevice)) !=
-        cudaSuccess) {
+            cudaSuccess ||
+        (e = start_upload()) != cudaSuccess) {
       err = cudaGetErrorString(e);
       return MPCORE_INTERNAL;
     }
@@ -748,21 +749,30 @@ class GpuShortSolver : public mpr::ShortSolver {
     if (e == cudaSuccess) e = grow_dev(&w.rres, w.rrcap, vb);
     if (e == cudaSuccess) e = grow_host(&w.hx, w.hcap, 2 * vb);
     if (e == cudaSuccess && A != w.stage) e = cudaErrorInvalidValue;
-    // A from the page-locked staging: asynchronous, overlapping the LU
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(w.rA, A, mb, cudaMemcpyHostToDevice, w.up);
-    if (e == cudaSuccess) {
-      std::memcpy(w.hx, b, vb);
-      e = cudaMemcpyAsync(w.rb, w.hx, vb, cudaMemcpyHostToDevice, w.up);
-    }
-    if (e == cudaSuccess) e = cudaEventRecord(w.up_done, w.up);
     if (e != cudaSuccess) {
       err = cudaGetErrorString(e);
       return MPCORE_INTERNAL;
     }
+    std::memcpy(w.hx, b, vb);
     rn_ = n;
     rp_ = p;
+    upload_pending_ = true;  // issued once the short matrix is on the GPU
     return MPCORE_OK;
+  }
+  // the long A (page-locked staging) and b to the device, asynchronously:
+  // started by factor() right after its own upload, so the two copies do
+  // not share the link and this one overlaps the LU
+  cudaError_t start_upload() {
+    if (!upload_pending_) return cudaSuccess;
+    upload_pending_ = false;
+    IrWorkspace &w = ir_ws();
+    const size_t mb = (size_t)rn_ * rn_ * LF_BYTES, vb = (size_t)rn_ * LF_BYTES;
+    cudaError_t e = cudaMemcpyAsync(w.rA, w.stage, mb, cudaMemcpyHostToDevice,
+                                    w.up);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(w.rb, w.hx, vb, cudaMemcpyHostToDevice, w.up);
+    if (e == cudaSuccess) e = cudaEventRecord(w.up_done, w.up);
+    return e;
   }
   int residual(const void *x, void *res, std::string &err) override {
     DevLock L;
@@ -770,10 +780,18 @@ class GpuShortSolver : public mpr::ShortSolver {
     IrWorkspace &w = ir_ws();
     Device &D = device();
     const size_t vb = (size_t)rn_ * LF_BYTES;
+    cudaError_t e = start_upload();  // (if factor() has not started it)
+    if (e != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
+    // b's upload reads the same page-locked buffer x goes through: let it
+    // finish first (a no-op after the first residual)
+    e = cudaStreamSynchronize(w.up);
     char *hx = static_cast<char *>(w.hx), *hres = hx + vb;
     std::memcpy(hx, x, vb);
-    cudaError_t e = cudaMemcpyAsync(w.rx, hx, vb, cudaMemcpyHostToDevice,
-                                    D.stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(w.rx, hx, vb, cudaMemcpyHostToDevice, D.stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(D.stream, w.up_done, 0);
     if (e == cudaSuccess)
       e = mpk::long_residual(rp_, rn_, w.rA, w.rx, w.rb, w.rres, D.stream);
@@ -821,6 +839,7 @@ class GpuShortSolver : public mpr::ShortSolver {
     return shared_;
   }
   int k_ = 0, n_ = 0, rn_ = 0, rp_ = 0;
+  bool upload_pending_ = false;
   bool tried_ = false;
   bool shared_ = false;  // buffers borrowed from ir_ws()
   double *a_ = nullptr, *b_ = nullptr, *x_ = nullptr;
