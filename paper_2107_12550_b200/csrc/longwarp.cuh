@@ -26,6 +26,10 @@ LWI uint64_t shfl(uint64_t v, int src) {
   return (src >= 0 && src < 32) ? r : 0ull;
 }
 LWI unsigned ballot(bool p) { return __ballot_sync(FULL, p); }
+// a condition every lane evaluates alike, as a vote: branches on it are
+// warp-uniform to the compiler too, so the shuffles after them need no
+// divergence handling
+LWI bool uni(bool p) { return __all_sync(FULL, p); }
 
 // limbs >> s bits (s >= 0)
 LWI uint64_t shr(uint64_t v, int s) {
@@ -52,7 +56,7 @@ LWI bool any_below(uint64_t v, int pos) {
 }
 LWI int top_bit(uint64_t v) {
   const unsigned nz = ballot(v != 0ull);
-  if (nz == 0u) return -1;
+  if (uni(nz == 0u)) return -1;
   const int h = 31 - __clz((int)nz);
   return 64 * h + 63 - __clzll((long long)shfl(v, h));
 }
@@ -80,7 +84,7 @@ LWI WV zero() { return WV{0ull, 0, 0}; }
 // limbs and the exponent adjustment; `sticky` marks bits lost before
 LWI void round_into(uint64_t S, int t, bool sticky, int p, int64_t base_exp,
                     WV &r) {
-  if (t < p) {  // fits: exact
+  if (uni(t < p)) {  // fits: exact
     const int sh = p - 1 - t;
     r.m = shl(S, sh);
     r.exp = base_exp - sh;
@@ -92,9 +96,9 @@ LWI void round_into(uint64_t S, int t, bool sticky, int p, int64_t base_exp,
   const bool half = get_bit(S, sh - 1);
   const bool below = sticky || any_below(S, sh - 1);
   const bool lsb = shfl(o, 0) & 1ull;
-  if (half && (below || lsb)) {
+  if (uni(half && (below || lsb))) {
     o = add_limbs(o, 0ull, true);
-    if (get_bit(o, p)) {  // rounded up to 2^p
+    if (uni(get_bit(o, p))) {  // rounded up to 2^p
       const int l = (p - 1) >> 6;
       o = lane_id() == l ? (1ull << ((p - 1) & 63)) : 0ull;
       r.exp += 1;
@@ -104,13 +108,13 @@ LWI void round_into(uint64_t S, int t, bool sticky, int p, int64_t base_exp,
 }
 
 LWI WV add(const WV &a, const WV &b, int p) {
-  if (a.sign == 0) return b;
-  if (b.sign == 0) return a;
+  if (uni(a.sign == 0)) return b;
+  if (uni(b.sign == 0)) return a;
   const bool ax = a.exp >= b.exp;
   const WV &x = ax ? a : b;
   const WV &y = ax ? b : a;
   const int64_t d64 = x.exp - y.exp;
-  if (d64 >= p + 3) return x;
+  if (uni(d64 >= p + 3)) return x;
   const int d = (int)d64;
   // frame: one guard limb below the mantissas
   const uint64_t X = shfl(x.m, lane_id() - 1);
@@ -119,13 +123,13 @@ LWI WV add(const WV &a, const WV &b, int p) {
   const uint64_t Y = shr(Yf, d);
   int sign = x.sign;
   uint64_t S;
-  if (x.sign == y.sign) {
+  if (uni(x.sign == y.sign)) {
     S = add_limbs(X, Y, false);
   } else {
     bool swap = false;
-    if (d == 0) {
+    if (uni(d == 0)) {
       const unsigned D = ballot(X != Y);
-      if (D == 0u) return zero();
+      if (uni(D == 0u)) return zero();
       const int h = 31 - __clz((int)D);
       swap = shfl(X, h) < shfl(Y, h);
       if (swap) sign = y.sign;
@@ -135,13 +139,13 @@ LWI WV add(const WV &a, const WV &b, int p) {
   WV r;
   r.sign = sign;
   const int t = top_bit(S);
-  if (t < 0) return zero();
+  if (uni(t < 0)) return zero();
   round_into(S, t, sticky, p, x.exp - 64, r);
   return r;
 }
 
 LWI WV mul(const WV &a, const WV &b, int p) {
-  if (a.sign == 0 || b.sign == 0) return zero();
+  if (uni(a.sign == 0 || b.sign == 0)) return zero();
   const int t = lane_id();
   // lane t: row products a_t * b_s for the 8 limbs s of b (limbs >= 8 are
   // zero for p <= 512); column t + s gets lo, t + s + 1 gets hi.  Round s:

@@ -40,7 +40,7 @@ long_residual_warp_kernel(const lf::DF *__restrict__ A,
                           const lf::DF *__restrict__ b,
                           lf::DF *__restrict__ res, int n, int p) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= n) return;  // warp-uniform
+  if (lw::uni(row >= n)) return;  // warp-uniform
   const int t = threadIdx.x & 31;
   auto load = [&](const lf::DF &v) {
     lw::WV w;
