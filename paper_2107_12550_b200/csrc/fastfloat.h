@@ -95,7 +95,11 @@ inline F round_to(int sign, const uint64_t *w, int n, int64_t e, int p) {
   if (L == 0) return r;
   r.sign = sign;
   if (L <= p) {
-    shl_into(w, n, p - L, r.m, NL);
+    if (L == p) {  // already p bits (the common case for inputs at p)
+      for (int i = 0; i < NL; ++i) r.m[i] = i < n ? w[i] : 0ull;
+    } else {
+      shl_into(w, n, p - L, r.m, NL);
+    }
     r.exp = e - (p - L);
     return r;
   }
@@ -347,64 +351,78 @@ template <int N> inline F mul_t(const F &a, const F &b, int p) {
 // peeled off exactly.  Returns false, leaving `out` undefined, when a head
 // would fall outside the normal binary64 range (the caller then takes the
 // generic path, which reproduces ldexp's subnormal rounding and overflow).
-template <int N> inline bool to_multicomp_t(F r, int k, int p, double *out) {
+template <int N>
+inline bool to_multicomp_t(const F &r0, int k, int p, double *out) {
+  // The value is sign * M * 2^e with the integer M in N limbs; each head is
+  // M's top 53 bits rounded to nearest even, and M keeps the exact signed
+  // remainder (no renormalisation: only its bit length is tracked).
+  uint64_t M[N];
+  for (int i = 0; i < N; ++i) M[i] = r0.m[i];
+  int sign = r0.sign;
+  const int64_t e = r0.exp;
+  int len = r0.sign == 0 ? 0 : p;
   for (int c = 0; c < k; ++c) {
-    if (r.sign == 0) {
+    if (len == 0) {
       out[c] = 0.0;
       continue;
     }
     uint64_t h;
-    int64_t E;  // head = h * 2^E, h <= 2^53
-    const int sh = p > 53 ? p - 53 : 0;
-    if (sh == 0) {
-      h = r.m[0];
-      E = r.exp;
+    int sh = 0;
+    bool up = false;
+    if (len <= 53) {
+      h = M[0];
     } else {
+      sh = len - 53;
       const int q = sh >> 6, rr = sh & 63;
-      const uint64_t lo = r.m[q], hi = q + 1 < N ? r.m[q + 1] : 0;
+      const uint64_t lo = M[q], hi = q + 1 < N ? M[q + 1] : 0;
       h = (rr ? (lo >> rr) | (hi << (64 - rr)) : lo) & ((1ull << 53) - 1ull);
       const int rb = sh - 1;
-      const bool half = (r.m[rb >> 6] >> (rb & 63)) & 1u;
-      bool below = false;
-      for (int l = 0; l < (rb >> 6) && !below; ++l) below = r.m[l] != 0;
-      if (!below && (rb & 63))
-        below = (r.m[rb >> 6] & ((1ull << (rb & 63)) - 1ull)) != 0;
-      if (half && (below || (h & 1u))) ++h;  // may reach 2^53 (exact)
-      E = r.exp + sh;
+      const bool half = (M[rb >> 6] >> (rb & 63)) & 1u;
+      if (half) {
+        bool below = (rb & 63) &&
+                     (M[rb >> 6] & ((1ull << (rb & 63)) - 1ull)) != 0;
+        for (int l = 0; l < (rb >> 6) && !below; ++l) below = M[l] != 0;
+        up = below || (h & 1u);
+      }
+      if (up) ++h;  // may reach 2^53 (exact)
     }
+    const int64_t E = e + sh;
     const int top = 63 - __builtin_clzll(h);
     if (E + top < -1022 || E + top > 1023) return false;
-    const double v = std::ldexp((double)h, (int)E);
-    out[c] = r.sign < 0 ? -v : v;
+    // h 2^E in the normal range: the binary64 bits directly (h != 0)
+    const int sh52 = 52 - top;  // h << sh52 has its top bit at 52 (may be < 0)
+    const uint64_t frac =
+        (sh52 >= 0 ? h << sh52 : h >> -sh52) & ((1ull << 52) - 1ull);
+    const uint64_t bits = ((uint64_t)(E + top + 1023) << 52) | frac |
+                          (sign < 0 ? (1ull << 63) : 0ull);
+    std::memcpy(&out[c], &bits, 8);
     if (c + 1 == k) break;
-    // r - head, exact: (m - (h << sh)) * 2^exp
-    uint64_t hv[N + 1], mm[N + 1], d[N + 1];
-    for (int i = 0; i <= N; ++i) hv[i] = 0;
-    {
-      const int q = sh >> 6, rr = sh & 63;
-      hv[q] |= h << rr;
-      if (rr && q + 1 <= N) hv[q + 1] |= h >> (64 - rr);
-    }
-    for (int i = 0; i < N; ++i) mm[i] = r.m[i];
-    mm[N] = 0;
-    int cmp = 0;
-    for (int i = N; i >= 0 && cmp == 0; --i)
-      if (mm[i] != hv[i]) cmp = mm[i] > hv[i] ? 1 : -1;
-    if (cmp == 0) {
-      r = F();
+    if (len <= 53) {  // the head took everything
+      len = 0;
       continue;
     }
-    const uint64_t *P = cmp > 0 ? mm : hv, *M = cmp > 0 ? hv : mm;
-    unsigned char bf = 0;
-    for (int i = 0; i <= N; ++i)
-      bf = _subborrow_u64(bf, P[i], M[i], (unsigned long long *)&d[i]);
-    const int t = top_bit<N + 1>(d);
-    F nr;
-    nr.sign = cmp > 0 ? r.sign : -r.sign;
-    for (int i = 0; i < NL; ++i) nr.m[i] = 0;
-    shl_into(d, N + 1, p - 1 - t, nr.m, N);
-    nr.exp = r.exp - (p - 1 - t);
-    r = nr;
+    // remainder: the low sh bits, or 2^sh minus them after rounding up
+    const int qs = sh >> 6, rs = sh & 63;
+    for (int i = 0; i < N; ++i) {
+      if (i > qs || (i == qs && rs == 0)) M[i] = 0;
+      else if (i == qs) M[i] &= (1ull << rs) - 1ull;
+    }
+    if (up) {
+      unsigned char cf = 1;  // two's complement, masked to sh bits
+      for (int i = 0; i < N; ++i)
+        cf = _addcarry_u64(cf, ~M[i], 0ull, (unsigned long long *)&M[i]);
+      for (int i = 0; i < N; ++i) {
+        if (i > qs || (i == qs && rs == 0)) M[i] = 0;
+        else if (i == qs) M[i] &= (1ull << rs) - 1ull;
+      }
+      sign = -sign;
+    }
+    len = 0;
+    for (int i = N - 1; i >= 0; --i)
+      if (M[i]) {
+        len = 64 * i + 64 - __builtin_clzll(M[i]);
+        break;
+      }
   }
   return true;
 }
