@@ -132,6 +132,13 @@ int32_t mpcore_object_info(uint64_t h, int32_t *kind, int32_t *k,
 /* host planar (k*rows*cols doubles) -> device object; count must match */
 int32_t mpcore_set_planes(uint64_t h, const double *planes, int64_t count);
 /* device object -> host planar; cap in doubles */
+/* Asynchronous mpcore_set_planes: the copy runs on its own stream and
+   overlaps the library's computation; every later call that touches the
+   device is ordered after it.  `planes` (page-locked for a truly
+   asynchronous copy) must stay unchanged until such a call returns.
+   Extension (pipelined solves). */
+int32_t mpcore_set_planes_async(uint64_t h, const double *planes,
+                                int64_t count);
 int32_t mpcore_get_planes(uint64_t h, double *out, int64_t cap);
 /* device-to-device copy between objects of identical shape */
 int32_t mpcore_copy(uint64_t src, uint64_t dst);

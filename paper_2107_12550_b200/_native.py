@@ -48,6 +48,7 @@ _PROTOS = {
     "mpcore_object_info": (_i32, [_u64, _ip, _ip, _ip, _ip]),
     "mpcore_set_planes": (_i32, [_u64, _dp, _i64]),
     "mpcore_get_planes": (_i32, [_u64, _dp, _i64]),
+    "mpcore_set_planes_async": (_i32, [_u64, _dp, _i64]),
     "mpcore_copy": (_i32, [_u64, _u64]),
     "mpcore_pivot_new": (_i32, [_i32, _ip, ctypes.POINTER(_u64)]),
     "mpcore_pivot_get": (_i32, [_u64, _ip, _i32]),
@@ -199,6 +200,18 @@ def release(h):
 def set_planes(h, planes):
     a = np.ascontiguousarray(planes, dtype=np.float64)
     check(lib().mpcore_set_planes(h, dptr(a), a.size), "set_planes")
+
+
+def set_planes_async(h, planes):
+    """Asynchronous upload (mpcore_set_planes_async): `planes` must be a
+    C-contiguous float64 array (page-locked for a truly asynchronous copy)
+    that stays unchanged until the next library call that uses the object
+    returns."""
+    if not (isinstance(planes, np.ndarray) and planes.dtype == np.float64
+            and planes.flags.c_contiguous):
+        raise ValueError("set_planes_async needs a C-contiguous float64 array")
+    check(lib().mpcore_set_planes_async(h, dptr(planes), planes.size),
+          "set_planes_async")
 
 
 def get_planes(h, shape, out=None):

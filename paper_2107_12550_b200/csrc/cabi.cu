@@ -43,7 +43,13 @@ struct Object {
   std::vector<int32_t> swaps;   // pivot record on host
   bool busy = false;            // mutation latch (ffi.py:96-105)
   std::unique_ptr<mpr::Report> report;
+  cudaEvent_t upload = nullptr; // last mpcore_set_planes_async copy
+  std::atomic<bool> upload_pending{false};  // not yet ordered before use
   ~Object() {
+    if (upload) {  // an asynchronous upload may still target d
+      cudaEventSynchronize(upload);
+      cudaEventDestroy(upload);
+    }
     if (d) cudaFree(d);
     if (dswaps) cudaFree(dswaps);
     if (dperm) cudaFree(dperm);
@@ -51,6 +57,10 @@ struct Object {
   int64_t count() const { return (int64_t)k * rows * cols; }
 };
 using ObjPtr = std::shared_ptr<Object>;
+
+// the library stream waits for the object's asynchronous upload, if one
+// is outstanding (every handle lookup below; defined after Device)
+void object_ready(Object &o);
 
 struct Table {
   std::mutex mu;
@@ -67,6 +77,7 @@ struct Table {
     std::lock_guard<std::mutex> g(mu);
     auto it = map.find(h);
     if (it == map.end() || (kind && it->second->kind != kind)) return nullptr;
+    object_ready(*it->second);
     return it->second;
   }
   bool drop(uint64_t h) {
@@ -80,6 +91,7 @@ struct Table {
     if (it == map.end() || it->second->kind != kind) return MPCORE_BAD_HANDLE;
     if (it->second->busy) return MPCORE_INTERNAL;
     it->second->busy = true;
+    object_ready(*it->second);
     o = it->second;
     return MPCORE_OK;
   }
@@ -116,11 +128,18 @@ struct Device {
   int swaps_cap = 0;
   double *aug = nullptr;      // [A | b] workspace of mpcore_solve_system
   size_t aug_bytes = 0;
+  // mpcore_set_planes_async: copies on their own stream
+  cudaStream_t copy = nullptr;
 };
 
 Device &device() {
   static Device d;
   return d;
+}
+
+void object_ready(Object &o) {
+  if (o.upload_pending.exchange(false))
+    cudaStreamWaitEvent(device().stream, o.upload, 0);
 }
 
 int cuda_fail(cudaError_t e, const char *where) {
@@ -1089,6 +1108,41 @@ int32_t mpcore_set_planes(uint64_t h, const double *planes, int64_t count) {
                                   cudaMemcpyHostToDevice, device().stream);
   if (e != cudaSuccess) return cuda_fail(e, "set_planes");
   return finish("set_planes");
+}
+
+// Asynchronous upload: the copy runs on its own stream, overlapping
+// whatever the library stream is computing; the next library call that
+// looks the object up orders the library stream after it.  The host buffer (page-locked for a
+// truly asynchronous copy) must stay unchanged until such a call returns.
+int32_t mpcore_set_planes_async(uint64_t h, const double *planes,
+                                int64_t count) {
+  ObjPtr o = table().get(h, 0);
+  if (!o || (o->kind != K_MATRIX && o->kind != K_VECTOR))
+    return MPCORE_BAD_HANDLE;
+  if (o->busy) return MPCORE_INTERNAL;  // latched by a running mutator
+  if (planes == nullptr || count != o->count()) return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  Device &D = device();
+  cudaError_t e = cudaSuccess;
+  if (!D.copy) e = cudaStreamCreateWithFlags(&D.copy, cudaStreamNonBlocking);
+  if (e == cudaSuccess && !o->upload)
+    e = cudaEventCreateWithFlags(&o->upload, cudaEventDisableTiming);
+  // after the library stream's queued work (which may still read the
+  // object), then the copy
+  cudaEvent_t after = nullptr;
+  if (e == cudaSuccess)
+    e = cudaEventCreateWithFlags(&after, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(after, D.stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(D.copy, after, 0);
+  if (after) cudaEventDestroy(after);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(o->d, planes, (size_t)count * sizeof(double),
+                        cudaMemcpyHostToDevice, D.copy);
+  if (e == cudaSuccess) e = cudaEventRecord(o->upload, D.copy);
+  if (e != cudaSuccess) return cuda_fail(e, "set_planes_async");
+  o->upload_pending.store(true);
+  return MPCORE_OK;
 }
 
 int32_t mpcore_get_planes(uint64_t h, double *out, int64_t cap) {
