@@ -140,6 +140,11 @@ int32_t mpcore_set_planes(uint64_t h, const double *planes, int64_t count);
 int32_t mpcore_set_planes_async(uint64_t h, const double *planes,
                                 int64_t count);
 int32_t mpcore_get_planes(uint64_t h, double *out, int64_t cap);
+/* Asynchronous mpcore_get_planes: on the copy stream, after the library's
+   queued work on the object; `out` (page-locked for a truly asynchronous
+   copy) is valid after mpcore_sync.  Later writes to the object wait for
+   the copy.  Extension (pipelined products). */
+int32_t mpcore_get_planes_async(uint64_t h, double *out, int64_t cap);
 /* device-to-device copy between objects of identical shape */
 int32_t mpcore_copy(uint64_t src, uint64_t dst);
 /* pivot record from a host swap list (PivotRecord(swaps), linalg.py:348-366) */

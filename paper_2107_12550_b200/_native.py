@@ -49,6 +49,7 @@ _PROTOS = {
     "mpcore_set_planes": (_i32, [_u64, _dp, _i64]),
     "mpcore_get_planes": (_i32, [_u64, _dp, _i64]),
     "mpcore_set_planes_async": (_i32, [_u64, _dp, _i64]),
+    "mpcore_get_planes_async": (_i32, [_u64, _dp, _i64]),
     "mpcore_copy": (_i32, [_u64, _u64]),
     "mpcore_pivot_new": (_i32, [_i32, _ip, ctypes.POINTER(_u64)]),
     "mpcore_pivot_get": (_i32, [_u64, _ip, _i32]),
@@ -212,6 +213,16 @@ def set_planes_async(h, planes):
         raise ValueError("set_planes_async needs a C-contiguous float64 array")
     check(lib().mpcore_set_planes_async(h, dptr(planes), planes.size),
           "set_planes_async")
+
+
+def get_planes_async(h, out):
+    """Asynchronous download into `out` (C-contiguous float64, page-locked
+    for a truly asynchronous copy); valid after sync()."""
+    if not (isinstance(out, np.ndarray) and out.dtype == np.float64
+            and out.flags.c_contiguous):
+        raise ValueError("get_planes_async needs a C-contiguous float64 array")
+    check(lib().mpcore_get_planes_async(h, dptr(out), out.size),
+          "get_planes_async")
 
 
 def get_planes(h, shape, out=None):

@@ -43,7 +43,7 @@ struct Object {
   std::vector<int32_t> swaps;   // pivot record on host
   bool busy = false;            // mutation latch (ffi.py:96-105)
   std::unique_ptr<mpr::Report> report;
-  cudaEvent_t upload = nullptr; // last mpcore_set_planes_async copy
+  cudaEvent_t upload = nullptr; // last asynchronous copy to / from d
   std::atomic<bool> upload_pending{false};  // not yet ordered before use
   ~Object() {
     if (upload) {  // an asynchronous upload may still target d
@@ -1145,6 +1145,37 @@ int32_t mpcore_set_planes_async(uint64_t h, const double *planes,
   return MPCORE_OK;
 }
 
+// Asynchronous download: after the library stream's queued work on the
+// object, on the copy stream; `out` is valid after mpcore_sync.  Later
+// library work that writes the object waits for the copy.
+int32_t mpcore_get_planes_async(uint64_t h, double *out, int64_t cap) {
+  ObjPtr o = table().get(h, 0);
+  if (!o || (o->kind != K_MATRIX && o->kind != K_VECTOR))
+    return MPCORE_BAD_HANDLE;
+  if (o->busy) return MPCORE_INTERNAL;
+  if (out == nullptr || cap < o->count()) return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  Device &D = device();
+  cudaError_t e = cudaSuccess;
+  if (!D.copy) e = cudaStreamCreateWithFlags(&D.copy, cudaStreamNonBlocking);
+  if (e == cudaSuccess && !o->upload)
+    e = cudaEventCreateWithFlags(&o->upload, cudaEventDisableTiming);
+  cudaEvent_t after = nullptr;
+  if (e == cudaSuccess)
+    e = cudaEventCreateWithFlags(&after, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(after, D.stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(D.copy, after, 0);
+  if (after) cudaEventDestroy(after);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out, o->d, (size_t)o->count() * sizeof(double),
+                        cudaMemcpyDeviceToHost, D.copy);
+  if (e == cudaSuccess) e = cudaEventRecord(o->upload, D.copy);
+  if (e != cudaSuccess) return cuda_fail(e, "get_planes_async");
+  o->upload_pending.store(true);
+  return MPCORE_OK;
+}
+
 int32_t mpcore_get_planes(uint64_t h, double *out, int64_t cap) {
   ObjPtr o = container(h);
   if (!o) return MPCORE_BAD_HANDLE;
@@ -1374,6 +1405,11 @@ int32_t mpcore_last_error(char *out, int32_t cap) {
 int32_t mpcore_sync(void) {
   DevLock L;
   if (L.st) return L.st;
+  Device &D = device();
+  if (D.copy) {  // asynchronous uploads / downloads too
+    cudaError_t e = cudaStreamSynchronize(D.copy);
+    if (e != cudaSuccess) return cuda_fail(e, "sync (copies)");
+  }
   return finish("sync");
 }
 

@@ -55,3 +55,31 @@ def test_async_upload_then_release_and_reuse():
     assert M2.download().tobytes() == A.tobytes()
     with pytest.raises(ValueError):
         nat.set_planes_async(M2.handle, A[:, :, ::2])
+
+
+@pytest.mark.parametrize("k,n", [(2, 130), (3, 64)])
+def test_async_download_pipelined_products(k, n):
+    # mat_mul with async uploads and downloads, two buffers per operand:
+    # every product equals the oracle's, and rewriting a C whose download
+    # is in flight waits for it
+    L = nat.lib()
+    systems = []
+    for s in (3, 4, 5):
+        A = gen.planes(k, (n, n), 0, n, s)
+        B = gen.planes(k, (n, n), 1, n, s)
+        hA, hB, hC = (nat.PinnedBuffer((k, n, n)) for _ in range(3))
+        hA.array[...] = A
+        hB.array[...] = B
+        systems.append((hA, hB, hC, oracle.gemm(A, B)))
+    EA = [DeviceMatrix(k, n, n) for _ in range(2)]
+    EB = [DeviceMatrix(k, n, n) for _ in range(2)]
+    EC = [DeviceMatrix(k, n, n) for _ in range(2)]
+    for i, (hA, hB, hC, _) in enumerate(systems):
+        nat.set_planes_async(EA[i % 2].handle, hA.array)
+        nat.set_planes_async(EB[i % 2].handle, hB.array)
+        nat.check(L.mpcore_mat_mul(EA[i % 2].handle, EB[i % 2].handle,
+                                   EC[i % 2].handle), "mm")
+        nat.get_planes_async(EC[i % 2].handle, hC.array)
+    nat.sync()
+    for hA, hB, hC, want in systems:
+        assert hC.array.tobytes() == want.tobytes()
