@@ -430,14 +430,20 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
     fro_exact = true;
     return true;
   };
+  std::vector<int> head_emax(T, INT_MIN);
+  std::vector<double> head_sum(T, 0.0);
   if (fast) {
-    // one pass: fixed-width copy and its k binary64 heads (bf_to_multicomp)
+    // one pass: fixed-width copy, its k binary64 heads (bf_to_multicomp)
+    // and, per thread, the largest head exponent with the sum of the heads'
+    // squares scaled by it (for the ||A||_F bounds below)
     std::vector<char> bad(T, 0);
     std::vector<std::thread> ws;
     for (int t = 0; t < T; ++t)
       ws.emplace_back([&, t] {
         const size_t a = nn * t / T, b = nn * (t + 1) / T;
         double c[4];
+        int hmax = INT_MIN;
+        double hsum = 0.0, hscale = 0.0;
         for (size_t e = a; e < b; ++e) {
           const ff::F v = ff::from_bf(Avals[e], pi);
           Af[e] = v;
@@ -447,7 +453,19 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
             break;
           }
           for (int q = 0; q < k; ++q) a_pl[(size_t)q * nn + e] = c[q];
+          if (c[0] != 0.0) {
+            const int eh = std::ilogb(c[0]);
+            if (eh > hmax) {  // rescale (powers of two)
+              if (hmax != INT_MIN) hsum = std::ldexp(hsum, 2 * (hmax - eh));
+              hmax = eh;
+              hscale = std::ldexp(1.0, -eh);
+            }
+            const double v = c[0] * hscale;
+            hsum += v * v;
+          }
         }
+        head_emax[t] = hmax;
+        head_sum[t] = hsum;
       });
     for (auto &w : ws) w.join();
     for (int t = 0; t < T; ++t)
@@ -468,44 +486,23 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
   // Rigorous bounds on ||A||_F from the binary64 heads (a_pl plane 0):
   // check_stop's threshold is monotone in ||A||_F, so a comparison that
   // falls outside [threshold(a_lo), threshold(a_hi)) is decided without the
-  // exact (sequentially rounded) sum, which keeps running on its thread
-  // and is waited for only when a comparison lands inside the bracket.
+  // exact (sequentially rounded) sum, which is formed only when a
+  // comparison lands inside the bracket (exact_fro).
   BF a_lo, a_hi;
   bool have_bounds = false;
   // MPCORE_REFINE_EXACT_FRO=1: always form the exact ||A||_F (tests)
   const bool force_exact = std::getenv("MPCORE_REFINE_EXACT_FRO") != nullptr;
   if (fast && !force_exact) {
-    // one chunk per thread, t-th chunk [nn t / T, nn (t + 1) / T)
-    auto par_chunks = [&](auto f) {
-      std::vector<std::thread> th;
-      for (int t = 0; t < T; ++t)
-        th.emplace_back([&, t] { f(t, nn * t / T, nn * (t + 1) / T); });
-      for (auto &x : th) x.join();
-    };
-    std::vector<int> emaxs(T, INT_MIN);
-    par_chunks([&](int t, size_t a, size_t b) {
-      int e = INT_MIN;
-      for (size_t q = a; q < b; ++q)
-        if (a_pl[q] != 0.0) e = std::max(e, std::ilogb(a_pl[q]));
-      emaxs[t] = e;
-    });
     int emax = INT_MIN;
-    for (int e : emaxs) emax = std::max(emax, e);
+    for (int e : head_emax) emax = std::max(emax, e);
     const double eps = (double)(nn + 64) * 0x1p-52 + 0x1p-50;
     // (heads far from the subnormal range: each within 2^-53 of its value,
     // and subnormal heads of tiny elements negligible against the slack)
     if (emax != INT_MIN && emax > -900 && eps < 0x1p-12) {
-      std::vector<double> part(T, 0.0);
-      par_chunks([&](int t, size_t a, size_t b) {
-        double acc = 0.0;
-        for (size_t q = a; q < b; ++q) {
-          const double v = std::ldexp(a_pl[q], -emax);
-          acc += v * v;
-        }
-        part[t] = acc;
-      });
       double S = 0.0;
-      for (double v : part) S += v;
+      for (int t = 0; t < T; ++t)
+        if (head_emax[t] != INT_MIN)
+          S += std::ldexp(head_sum[t], 2 * (head_emax[t] - emax));
       // heads: relative error 2^-53 each (squares 2^-52); sums of nn terms
       // (nn + T) u; underflowed squares at most nn 2^-1022 in total
       const double lo2 = S * (1.0 - eps) - (double)nn * 0x1p-1000;
