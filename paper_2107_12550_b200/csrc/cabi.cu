@@ -735,6 +735,72 @@ class GpuShortSolver : public mpr::ShortSolver {
       return MPCORE_INTERNAL;
     }
     (void)D;
+    ld_ = n;
+    return MPCORE_OK;
+  }
+  // factor + first solve in one call: b rides along the factorisation as
+  // column n of [A | b] (its forward substitution), then the back
+  // substitution (solve_augmented_locked, bitwise factor + solve); the
+  // factors stay in place with row stride n + 1 for the later solves
+  int factor_solve(int k, int n, const double *a, const std::vector<double> &b,
+                   std::vector<double> &x, std::string &err) override {
+    k_ = k;
+    n_ = n;
+    DevLock L;
+    if (L.st) { err = g_err; return L.st; }
+    Device &D = device();
+    cudaError_t e = cudaSuccess;
+    const size_t plane = (size_t)n * (n + 1);
+    const size_t mb = (size_t)k * plane * sizeof(double), vb = (size_t)k * n * 8;
+    if (a_ == nullptr && claim()) {
+      IrWorkspace &w = ir_ws();
+      if ((e = grow_dev((void **)&w.a, w.acap, mb)) == cudaSuccess &&
+          (e = grow_dev((void **)&w.b, w.bcap, vb)) == cudaSuccess &&
+          (e = grow_dev((void **)&w.x, w.xcap, vb)) == cudaSuccess)
+        e = grow_dev((void **)&w.perm, w.pcap, (size_t)n * 4);
+      a_ = w.a;
+      b_ = w.b;
+      x_ = w.x;
+      perm_ = w.perm;
+    } else if (a_ == nullptr) {
+      if ((e = cudaMalloc(&a_, mb)) == cudaSuccess &&
+          (e = cudaMalloc(&b_, vb)) == cudaSuccess &&
+          (e = cudaMalloc(&x_, vb)) == cudaSuccess)
+        e = cudaMalloc(&perm_, (size_t)n * 4);
+    }
+    for (int c = 0; c < k && e == cudaSuccess; ++c) {
+      e = cudaMemcpy2DAsync(a_ + c * plane, (n + 1) * 8, a + (size_t)c * n * n,
+                            (size_t)n * 8, (size_t)n * 8, n,
+                            cudaMemcpyHostToDevice, D.stream);
+      if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(a_ + c * plane + n, (n + 1) * 8,
+                              b.data() + (size_t)c * n, 8, 8, n,
+                              cudaMemcpyHostToDevice, D.stream);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(D.stream);
+    if (e == cudaSuccess) e = start_upload();
+    if (e != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
+    std::vector<int32_t> swaps;
+    int32_t step = -1;
+    int st = solve_augmented_locked(k, n, a_, n + 1, (int64_t)plane, x_, 0,
+                                    swaps, &step);
+    if (st) { err = g_err; return st; }
+    ld_ = n + 1;
+    x.resize((size_t)k * n);
+    std::vector<int32_t> order(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    for (int j = 0; j < n; ++j)
+      if (swaps[j] != j) std::swap(order[j], order[swaps[j]]);
+    if ((e = cudaMemcpy(x.data(), x_, vb, cudaMemcpyDeviceToHost)) !=
+            cudaSuccess ||
+        (e = cudaMemcpy(perm_, order.data(), (size_t)n * 4,
+                        cudaMemcpyHostToDevice)) != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
     return MPCORE_OK;
   }
   // ---- the long residual on the device (residual.cu) ----
@@ -833,7 +899,7 @@ class GpuShortSolver : public mpr::ShortSolver {
     size_t vb = (size_t)k_ * n_ * 8;
     cudaError_t e = cudaMemcpyAsync(b_, b.data(), vb, cudaMemcpyHostToDevice,
                                     D.stream);
-    mpk::MatView v{a_, n_, (int64_t)n_ * n_};
+    mpk::MatView v{a_, ld_, (int64_t)n_ * ld_};
     if (e == cudaSuccess)
       e = mpk::lu_solve(k_, n_, v, perm_, b_, x_, D.sw, D.stream);
     x.resize((size_t)k_ * n_);
@@ -858,6 +924,7 @@ class GpuShortSolver : public mpr::ShortSolver {
     return shared_;
   }
   int k_ = 0, n_ = 0, rn_ = 0, rp_ = 0;
+  int ld_ = 0;  // row stride of the factors (n, or n + 1 after factor_solve)
   bool upload_pending_ = false;
   bool tried_ = false;
   bool shared_ = false;  // buffers borrowed from ir_ws()

@@ -531,9 +531,10 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
     }
   }
   const auto t1 = Clock::now();
-  if ((st = S.factor(k, n, a_pl.p, err))) return st;
+  // the factorisation and the first solve (b along the LU on the GPU)
+  if ((st = S.factor_solve(k, n, a_pl.p, b_pl, x_pl, err))) return st;
   const auto t2 = Clock::now();
-  plog.mark("factor");
+  plog.mark("factor + first solve");
   double t_solve = 0, t_res = 0;
   auto timed_solve = [&](const std::vector<double> &rhs) {
     const auto a = Clock::now();
@@ -541,8 +542,6 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
     t_solve += secs(a, Clock::now());
     return r;
   };
-  if ((st = timed_solve(b_pl))) return st;
-  plog.mark("first solve");
   // bf_from_multicomp at p_in, then into the working precision
   auto lift = [&](const std::vector<double> &pl, std::vector<BF> &x) {
     x.resize(n);
@@ -712,7 +711,7 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
   out.stop_reason = reason;
   out.solution = x;
   out.prec = p;
-  // convert, factor, refinement loop (incl. first solve), residuals, solves
+  // convert, factor (+ the first solve), refinement loop, residuals, solves
   out.timings = {secs(t0, t1), secs(t1, t2), secs(t2, t3), t_res, t_solve};
   return 0;
 }

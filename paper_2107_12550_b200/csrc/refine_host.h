@@ -34,6 +34,14 @@ class ShortSolver {
                      std::string &err) = 0;
   virtual int solve(const std::vector<double> &b_planes,
                     std::vector<double> &x_planes, std::string &err) = 0;
+  // factor and the first solve in one call (a GPU solver carries b along
+  // the factorisation); the same results as factor() + solve()
+  virtual int factor_solve(int k, int n, const double *a_planes,
+                           const std::vector<double> &b_planes,
+                           std::vector<double> &x_planes, std::string &err) {
+    const int st = factor(k, n, a_planes, err);
+    return st ? st : solve(b_planes, x_planes, err);
+  }
   // Optional: the long residual b - A x on the device.
   // Values travel as fixed-width long floats (fastfloat.h ff::F, p <= 512).
   virtual bool residual_supported(int p) { return false; }
