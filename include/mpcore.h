@@ -166,7 +166,8 @@ int32_t mpcore_mat_mul(uint64_t a, uint64_t b, uint64_t c);
 /* y = A*x, mat_vec (linalg.py:545-574) */
 int32_t mpcore_mat_vec(uint64_t a, uint64_t x, uint64_t y);
 /* out = x op y elementwise: op 0 add, 1 mul (linalg.py:648-673), 2 div
- * (mcfloat.py:304-318; a zero divisor head returns 6) */
+ * (mcfloat.py:304-318; a zero divisor head returns 6), 3 sqrt of x
+ * (_sqrt_t, mcfloat.py:324-340; y is not read; a negative head returns 6) */
 int32_t mpcore_elementwise(int32_t op, uint64_t x, uint64_t y, uint64_t out);
 /* y <- y + x*alpha (axpy_batch, linalg.py:624-645); alpha: k doubles */
 int32_t mpcore_axpy(const double *alpha, int32_t k, uint64_t x, uint64_t y);

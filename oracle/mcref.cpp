@@ -206,6 +206,37 @@ template <int K> static void divk(const double *a, const double *b, double *o) {
   compress(o, K);
 }
 
+// _sqrt_t (mcfloat.py:324-340); caller guarantees a[0] >= 0.
+template <int K> static void sqrtk(const double *a, double *o) {
+  if (a[0] == 0.0) {
+    for (int c = 0; c < K; ++c) o[c] = 0.0;
+    return;
+  }
+  const int steps = K == 4 ? 3 : 2;  // _SQRT_STEPS
+  double one[K] = {}, y[K] = {};
+  one[0] = 1.0;
+  y[0] = 1.0 / std::sqrt(a[0]);
+  for (int it = 0; it < steps; ++it) {
+    double yy[K], ayy[K], r[K], yr[K], h[K], ny[K];
+    mul<K>(y, y, yy);
+    mul<K>(a, yy, ayy);
+    for (int c = 0; c < K; ++c) ayy[c] = -ayy[c];
+    add<K>(one, ayy, r);
+    mul<K>(y, r, yr);
+    mul_scalar<K>(yr, 0.5, h);
+    add<K>(y, h, ny);
+    for (int c = 0; c < K; ++c) y[c] = ny[c];
+  }
+  double s[K], ss[K], e[K], yh[K], ey[K];
+  mul<K>(a, y, s);
+  mul<K>(s, s, ss);
+  for (int c = 0; c < K; ++c) ss[c] = -ss[c];
+  add<K>(a, ss, e);
+  mul_scalar<K>(y, 0.5, yh);
+  mul<K>(e, yh, ey);
+  add<K>(s, ey, o);
+}
+
 // --------------------------------------------------------- dense kernels ----
 // Element (i, j) of plane c: p[c * plane + i * ld + j].
 
@@ -467,7 +498,7 @@ static void gemm(int m, int kk, int nn, const double *A, const double *B,
 }
 
 // Elementwise kernels over n lanes (linalg.py:624-673, mcfloat.py:304-318).
-// op: 0 add(x, y), 1 mul(x, y), 2 div(x, y), 3 axpy y = add(y, mul(x, alpha))
+// op: 0 add(x, y), 1 mul(x, y), 2 div(x, y), 4 sqrt(x) (y unused)
 template <int K>
 static void elementwise(int op, int64_t n, const double *x, const double *y,
                         double *out) {
@@ -477,7 +508,8 @@ static void elementwise(int op, int64_t n, const double *x, const double *y,
     for (int c = 0; c < K; ++c) { a[c] = x[c * n + i]; b[c] = y[c * n + i]; }
     if (op == 0) add<K>(a, b, o);
     else if (op == 1) mul<K>(a, b, o);
-    else divk<K>(a, b, o);
+    else if (op == 2) divk<K>(a, b, o);
+    else sqrtk<K>(a, o);
     for (int c = 0; c < K; ++c) out[c * n + i] = o[c];
   }
 }
@@ -517,7 +549,7 @@ int mcref_two_prod(int64_t n, const double *a, const double *b, double *p,
 }
 int mcref_elementwise(int k, int op, int64_t n, const double *x,
                       const double *y, double *out) {
-  if (op < 0 || op > 2) return 2;
+  if (op < 0 || op > 4 || op == 3) return 2;
   DISPATCH(k, elementwise<K>(op, n, x, y, out));
   return 0;
 }

@@ -19,9 +19,12 @@ from .linalg import (  # noqa: F401
     elementwise_add_batch, elementwise_div_batch, elementwise_mul_batch,
     lu_factor_pp, lu_solve, mat_mul_blocked, mat_norm_fro, mat_vec,
     max_rel_err, vec_norm2)
-from .longfloat import LF, PrecisionContext  # noqa: F401
+from .bigfloat import (  # noqa: F401
+    BigFloat, PrecisionContext, bf_from_multicomp, bf_parse_decimal,
+    bf_to_multicomp)
+from .longfloat import LF  # noqa: F401
 from .mcfloat import (  # noqa: F401
-    MultiComp, mc_add, mc_div, mc_mul, mc_sub)
+    MultiComp, mc_add, mc_div, mc_mul, mc_sqrt, mc_sub)
 from .refine import (  # noqa: F401
     RefineConfig, RefineReport, check_stop, iterative_refinement,
     iterative_refinement_td_mp)
@@ -42,8 +45,9 @@ __all__ = [
     "MpcoreError", "ArithmeticOverflowError", "DivideByZeroError",
     "DomainError", "SingularMatrixError", "DimensionError", "ParseError",
     "GenerationError",
-    "MultiComp", "mc_add", "mc_sub", "mc_mul", "mc_div",
-    "LF", "PrecisionContext",
+    "MultiComp", "mc_add", "mc_sub", "mc_mul", "mc_div", "mc_sqrt",
+    "BigFloat", "PrecisionContext", "bf_parse_decimal",
+    "bf_to_multicomp", "bf_from_multicomp", "LF",
     "McDomain", "BfDomain", "Vector", "DenseMatrix", "PivotRecord",
     "lu_factor_pp", "lu_solve", "mat_vec", "mat_mul_blocked",
     "vec_norm2", "mat_norm_fro", "max_rel_err",

@@ -203,6 +203,12 @@ def set_planes(h, planes):
     check(lib().mpcore_set_planes(h, dptr(a), a.size), "set_planes")
 
 
+# host arrays an asynchronous copy still reads or writes: kept alive here
+# until sync() returns (a dropped array would otherwise be freed under the
+# DMA)
+_inflight = []
+
+
 def set_planes_async(h, planes):
     """Asynchronous upload (mpcore_set_planes_async): `planes` must be a
     C-contiguous float64 array (page-locked for a truly asynchronous copy)
@@ -213,6 +219,7 @@ def set_planes_async(h, planes):
         raise ValueError("set_planes_async needs a C-contiguous float64 array")
     check(lib().mpcore_set_planes_async(h, dptr(planes), planes.size),
           "set_planes_async")
+    _inflight.append(planes)
 
 
 def get_planes_async(h, out):
@@ -223,6 +230,7 @@ def get_planes_async(h, out):
         raise ValueError("get_planes_async needs a C-contiguous float64 array")
     check(lib().mpcore_get_planes_async(h, dptr(out), out.size),
           "get_planes_async")
+    _inflight.append(out)
 
 
 def get_planes(h, shape, out=None):
@@ -341,6 +349,7 @@ def sm_count():
 
 def sync():
     check(lib().mpcore_sync(), "sync")
+    del _inflight[:]
 
 
 class StreamTimer:

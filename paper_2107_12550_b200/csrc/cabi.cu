@@ -44,7 +44,10 @@ struct Object {
   bool busy = false;            // mutation latch (ffi.py:96-105)
   std::unique_ptr<mpr::Report> report;
   cudaEvent_t upload = nullptr; // last asynchronous copy to / from d
-  std::atomic<bool> upload_pending{false};  // not yet ordered before use
+  // an asynchronous copy was recorded in `upload` and the library stream
+  // has not yet been made to wait for it; set and cleared only under the
+  // device lock
+  std::atomic<bool> upload_pending{false};
   ~Object() {
     if (upload) {  // an asynchronous upload may still target d
       cudaEventSynchronize(upload);
@@ -58,9 +61,14 @@ struct Object {
 };
 using ObjPtr = std::shared_ptr<Object>;
 
-// the library stream waits for the object's asynchronous upload, if one
-// is outstanding (every handle lookup below; defined after Device)
-void object_ready(Object &o);
+// Every handle lookup notes objects with an outstanding asynchronous copy;
+// the next DevLock taken by the same thread (before it queues any work on
+// the library stream, and never while another thread captures that stream
+// into a graph) makes the library stream wait for those copies.
+thread_local std::vector<std::shared_ptr<Object>> g_touched;
+void object_ready(const std::shared_ptr<Object> &o) {
+  if (o->upload_pending.load()) g_touched.push_back(o);
+}
 
 struct Table {
   std::mutex mu;
@@ -77,7 +85,7 @@ struct Table {
     std::lock_guard<std::mutex> g(mu);
     auto it = map.find(h);
     if (it == map.end() || (kind && it->second->kind != kind)) return nullptr;
-    object_ready(*it->second);
+    object_ready(it->second);
     return it->second;
   }
   bool drop(uint64_t h) {
@@ -91,7 +99,7 @@ struct Table {
     if (it == map.end() || it->second->kind != kind) return MPCORE_BAD_HANDLE;
     if (it->second->busy) return MPCORE_INTERNAL;
     it->second->busy = true;
-    object_ready(*it->second);
+    object_ready(it->second);
     o = it->second;
     return MPCORE_OK;
   }
@@ -135,11 +143,6 @@ struct Device {
 Device &device() {
   static Device d;
   return d;
-}
-
-void object_ready(Object &o) {
-  if (o.upload_pending.exchange(false))
-    cudaStreamWaitEvent(device().stream, o.upload, 0);
 }
 
 int cuda_fail(cudaError_t e, const char *where) {
@@ -207,10 +210,27 @@ cudaEvent_t *event_slots() {
   return slots;
 }
 
+// Holds the device lock; orders the library stream after the asynchronous
+// copies of the objects this thread looked up (g_touched).  A flag is
+// cleared only once its stream wait has been queued successfully.
 struct DevLock {
   std::unique_lock<std::mutex> lk;
   int st;
-  DevLock() : lk(device().mu) { st = ensure_device_locked(); }
+  DevLock() : lk(device().mu) {
+    st = ensure_device_locked();
+    std::vector<std::shared_ptr<Object>> touched;
+    touched.swap(g_touched);
+    if (st) return;
+    for (auto &o : touched) {
+      if (!o->upload_pending.load()) continue;
+      cudaError_t e = cudaStreamWaitEvent(device().stream, o->upload, 0);
+      if (e != cudaSuccess) {
+        st = cuda_fail(e, "wait for asynchronous copy");
+        return;
+      }
+      o->upload_pending.store(false);
+    }
+  }
 };
 
 int finish(const char *where) {
@@ -275,6 +295,7 @@ int64_t elem_index(const ObjPtr &o, int i, int j) {
   return o->kind == K_MATRIX ? (int64_t)i * o->cols + j : (int64_t)i;
 }
 
+// (device lock held by the caller)
 int make_pivot(const std::vector<int32_t> &swaps, uint64_t *out) {
   auto p = std::make_shared<Object>();
   p->kind = K_PIVOT;
@@ -283,8 +304,10 @@ int make_pivot(const std::vector<int32_t> &swaps, uint64_t *out) {
   p->swaps = swaps;
   cudaError_t e = cudaMalloc(&p->dswaps, swaps.size() * sizeof(int32_t));
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(pivot)");
-  e = cudaMemcpy(p->dswaps, swaps.data(), swaps.size() * sizeof(int32_t),
-                 cudaMemcpyHostToDevice);
+  // uploads on the library stream (where every solve reads them); the
+  // host vectors live until finish() below has seen them land
+  e = cudaMemcpyAsync(p->dswaps, swaps.data(), swaps.size() * sizeof(int32_t),
+                      cudaMemcpyHostToDevice, device().stream);
   if (e != cudaSuccess) return cuda_fail(e, "pivot upload");
   // permutation(): position i holds original row order[i] (linalg.py:361-366)
   std::vector<int32_t> order(swaps.size());
@@ -293,9 +316,11 @@ int make_pivot(const std::vector<int32_t> &swaps, uint64_t *out) {
     if (swaps[j] != (int32_t)j) std::swap(order[j], order[swaps[j]]);
   e = cudaMalloc(&p->dperm, order.size() * sizeof(int32_t));
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(perm)");
-  e = cudaMemcpy(p->dperm, order.data(), order.size() * sizeof(int32_t),
-                 cudaMemcpyHostToDevice);
+  e = cudaMemcpyAsync(p->dperm, order.data(), order.size() * sizeof(int32_t),
+                      cudaMemcpyHostToDevice, device().stream);
   if (e != cudaSuccess) return cuda_fail(e, "perm upload");
+  int st = finish("pivot upload");
+  if (st) return st;
   *out = table().put(p);
   return MPCORE_OK;
 }
@@ -671,6 +696,7 @@ class GpuShortSolver : public mpr::ShortSolver {
       return;
     }
     if (a_ || perm_ || b_ || x_) {
+      // (owned buffers; the shared ones stay in ir_ws() for the next call)
       DevLock L;
       if (a_) cudaFree(a_);
       if (perm_) cudaFree(perm_);
@@ -687,30 +713,13 @@ class GpuShortSolver : public mpr::ShortSolver {
     Device &D = device();
     cudaError_t e = cudaSuccess;
     size_t mb = (size_t)k * n * n * sizeof(double), vb = (size_t)k * n * 8;
-    if (a_ == nullptr && claim()) {
-      IrWorkspace &w = ir_ws();
-      if ((e = grow_dev((void **)&w.a, w.acap, mb)) == cudaSuccess &&
-          (e = grow_dev((void **)&w.b, w.bcap, vb)) == cudaSuccess &&
-          (e = grow_dev((void **)&w.x, w.xcap, vb)) == cudaSuccess)
-        e = grow_dev((void **)&w.perm, w.pcap, (size_t)n * 4);
-      if (e != cudaSuccess) {
-        err = cudaGetErrorString(e);
-        return MPCORE_INTERNAL;
-      }
-      a_ = w.a;
-      b_ = w.b;
-      x_ = w.x;
-      perm_ = w.perm;
-    } else if (a_ == nullptr &&
-               ((e = cudaMalloc(&a_, mb)) != cudaSuccess ||
-               (e = cudaMalloc(&b_, vb)) != cudaSuccess ||
-               (e = cudaMalloc(&x_, vb)) != cudaSuccess ||
-               (e = cudaMalloc(&perm_, (size_t)n * 4)) != cudaSuccess)) {
+    if ((e = ensure_buffers(mb, vb, (size_t)n * 4)) != cudaSuccess) {
       err = cudaGetErrorString(e);
       return MPCORE_INTERNAL;
     }
-    if ((e = cudaMemcpy(a_, a, mb, cudaMemcpyHostToDevice)) !=
+    if ((e = cudaMemcpyAsync(a_, a, mb, cudaMemcpyHostToDevice, D.stream)) !=
             cudaSuccess ||
+        (e = cudaStreamSynchronize(D.stream)) != cudaSuccess ||
         (e = start_upload()) != cudaSuccess) {
       err = cudaGetErrorString(e);
       return MPCORE_INTERNAL;
@@ -729,12 +738,14 @@ class GpuShortSolver : public mpr::ShortSolver {
     for (int i = 0; i < n; ++i) order[i] = i;
     for (int j = 0; j < n; ++j)
       if (swaps[j] != j) std::swap(order[j], order[swaps[j]]);
-    if ((e = cudaMemcpy(perm_, order.data(), (size_t)n * 4,
-                        cudaMemcpyHostToDevice)) != cudaSuccess) {
+    // ordered on the library stream (the solves read perm_ there); the
+    // host vector stays alive until the copy has landed
+    if ((e = cudaMemcpyAsync(perm_, order.data(), (size_t)n * 4,
+                             cudaMemcpyHostToDevice, D.stream)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(D.stream)) != cudaSuccess) {
       err = cudaGetErrorString(e);
       return MPCORE_INTERNAL;
     }
-    (void)D;
     ld_ = n;
     return MPCORE_OK;
   }
@@ -752,22 +763,7 @@ class GpuShortSolver : public mpr::ShortSolver {
     cudaError_t e = cudaSuccess;
     const size_t plane = (size_t)n * (n + 1);
     const size_t mb = (size_t)k * plane * sizeof(double), vb = (size_t)k * n * 8;
-    if (a_ == nullptr && claim()) {
-      IrWorkspace &w = ir_ws();
-      if ((e = grow_dev((void **)&w.a, w.acap, mb)) == cudaSuccess &&
-          (e = grow_dev((void **)&w.b, w.bcap, vb)) == cudaSuccess &&
-          (e = grow_dev((void **)&w.x, w.xcap, vb)) == cudaSuccess)
-        e = grow_dev((void **)&w.perm, w.pcap, (size_t)n * 4);
-      a_ = w.a;
-      b_ = w.b;
-      x_ = w.x;
-      perm_ = w.perm;
-    } else if (a_ == nullptr) {
-      if ((e = cudaMalloc(&a_, mb)) == cudaSuccess &&
-          (e = cudaMalloc(&b_, vb)) == cudaSuccess &&
-          (e = cudaMalloc(&x_, vb)) == cudaSuccess)
-        e = cudaMalloc(&perm_, (size_t)n * 4);
-    }
+    e = ensure_buffers(mb, vb, (size_t)n * 4);
     for (int c = 0; c < k && e == cudaSuccess; ++c) {
       e = cudaMemcpy2DAsync(a_ + c * plane, (n + 1) * 8, a + (size_t)c * n * n,
                             (size_t)n * 8, (size_t)n * 8, n,
@@ -794,10 +790,11 @@ class GpuShortSolver : public mpr::ShortSolver {
     for (int i = 0; i < n; ++i) order[i] = i;
     for (int j = 0; j < n; ++j)
       if (swaps[j] != j) std::swap(order[j], order[swaps[j]]);
-    if ((e = cudaMemcpy(x.data(), x_, vb, cudaMemcpyDeviceToHost)) !=
-            cudaSuccess ||
-        (e = cudaMemcpy(perm_, order.data(), (size_t)n * 4,
-                        cudaMemcpyHostToDevice)) != cudaSuccess) {
+    if ((e = cudaMemcpyAsync(x.data(), x_, vb, cudaMemcpyDeviceToHost,
+                             D.stream)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(perm_, order.data(), (size_t)n * 4,
+                             cudaMemcpyHostToDevice, D.stream)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(D.stream)) != cudaSuccess) {
       err = cudaGetErrorString(e);
       return MPCORE_INTERNAL;
     }
@@ -914,6 +911,31 @@ class GpuShortSolver : public mpr::ShortSolver {
   }
 
  private:
+  // device buffers for a factorisation of mb matrix bytes, vb vector bytes
+  // and pb permutation bytes: the shared workspace (grow-only) if this
+  // solver holds it, else buffers owned by the solver; both are re-checked
+  // on every factor / factor_solve, so a larger n or the n x (n+1) layout
+  // after an n x n factor never writes past an allocation
+  cudaError_t ensure_buffers(size_t mb, size_t vb, size_t pb) {
+    cudaError_t e = cudaSuccess;
+    if (claim()) {
+      IrWorkspace &w = ir_ws();
+      if ((e = grow_dev((void **)&w.a, w.acap, mb)) == cudaSuccess &&
+          (e = grow_dev((void **)&w.b, w.bcap, vb)) == cudaSuccess &&
+          (e = grow_dev((void **)&w.x, w.xcap, vb)) == cudaSuccess)
+        e = grow_dev((void **)&w.perm, w.pcap, pb);
+      a_ = w.a;
+      b_ = w.b;
+      x_ = w.x;
+      perm_ = w.perm;
+      return e;
+    }
+    if ((e = grow_dev((void **)&a_, acap_, mb)) == cudaSuccess &&
+        (e = grow_dev((void **)&b_, bcap_, vb)) == cudaSuccess &&
+        (e = grow_dev((void **)&x_, xcap_, vb)) == cudaSuccess)
+      e = grow_dev((void **)&perm_, pcap_, pb);
+    return e;
+  }
   // the shared workspace, if no other refinement holds it (asked once)
   bool claim() {
     if (!tried_) {
@@ -930,6 +952,7 @@ class GpuShortSolver : public mpr::ShortSolver {
   bool shared_ = false;  // buffers borrowed from ir_ws()
   double *a_ = nullptr, *b_ = nullptr, *x_ = nullptr;
   int32_t *perm_ = nullptr;
+  size_t acap_ = 0, bcap_ = 0, xcap_ = 0, pcap_ = 0;  // owned buffers only
 };
 }  // namespace
 
@@ -1355,21 +1378,29 @@ int32_t mpcore_mat_vec(uint64_t a, uint64_t x, uint64_t y) {
 int32_t mpcore_elementwise(int32_t op, uint64_t x, uint64_t y, uint64_t out) {
   ObjPtr X = container(x), Y = container(y), O = container(out);
   if (!X || !Y || !O) return MPCORE_BAD_HANDLE;
-  if (op < 0 || op > 2) return MPCORE_BAD_DIMENSION;
+  if (op < 0 || op > 3) return MPCORE_BAD_DIMENSION;
   if (X->k != Y->k || O->k != X->k || X->count() != Y->count() ||
       O->count() != X->count())
     return MPCORE_BAD_DIMENSION;
   DevLock L;
   if (L.st) return L.st;
-  if (op == 2) {  // division by an exact zero raises in the reference
-    std::vector<double> heads(Y->count() / Y->k);
-    cudaError_t e = cudaMemcpyAsync(heads.data(), Y->d, heads.size() * sizeof(double),
+  if (op >= 2) {
+    // division by an exact zero and the square root of a negative value
+    // raise in the reference (mcfloat.py:309-310, 325-326)
+    const ObjPtr &chk = op == 2 ? Y : X;
+    std::vector<double> heads(chk->count() / chk->k);
+    cudaError_t e = cudaMemcpyAsync(heads.data(), chk->d,
+                                    heads.size() * sizeof(double),
                                     cudaMemcpyDeviceToHost, device().stream);
-    if (e != cudaSuccess) return cuda_fail(e, "div check");
-    int st = finish("div check");
+    if (e != cudaSuccess) return cuda_fail(e, "operand check");
+    int st = finish("operand check");
     if (st) return st;
-    for (double v : heads)
-      if (v == 0.0) return fail(MPCORE_INTERNAL, "division by zero");
+    for (double v : heads) {
+      if (op == 2 && v == 0.0)
+        return fail(MPCORE_INTERNAL, "division by zero");
+      if (op == 3 && v < 0.0)
+        return fail(MPCORE_INTERNAL, "square root of a negative value");
+    }
   }
   cudaError_t e = mpk::elementwise(X->k, op, X->count() / X->k, X->d, Y->d,
                                    O->d, device().stream);

@@ -1,5 +1,6 @@
 // Elementwise batch kernels (linalg.py:624-673: axpy_batch,
-// elementwise_add/mul_batch), elementwise division (mcfloat.py:304-318),
+// elementwise_add/mul_batch), elementwise division (mcfloat.py:304-318) and
+// square root (mcfloat.py:324-340, mc_sqrt 596-601),
 // mat_vec (linalg.py:545-574) and the seeded planar input generator.
 #include "internal.h"
 #include "mc.cuh"
@@ -20,11 +21,12 @@ ew_kernel(int64_t n, const double *__restrict__ x,
 #pragma unroll
     for (int c = 0; c < K; ++c) {
       a[c] = x[c * n + i];
-      b[c] = y[c * n + i];
+      b[c] = OP == 3 ? 0.0 : y[c * n + i];
     }
     if constexpr (OP == 0) mc::add<K>(a, b, o);
     else if constexpr (OP == 1) mc::mul<K>(a, b, o);
-    else mc::div<K>(a, b, o);
+    else if constexpr (OP == 2) mc::div<K>(a, b, o);
+    else mc::sqrt<K>(a, o);  // (unary: y is not read)
 #pragma unroll
     for (int c = 0; c < K; ++c) out[c * n + i] = o[c];
   }
@@ -181,7 +183,8 @@ cudaError_t ew_dispatch(int op, int64_t n, const double *x, const double *y,
   int g = grid_for(n);
   if (op == 0) ew_kernel<K, 0><<<g, EW_THREADS, 0, s>>>(n, x, y, out);
   else if (op == 1) ew_kernel<K, 1><<<g, EW_THREADS, 0, s>>>(n, x, y, out);
-  else ew_kernel<K, 2><<<g, EW_THREADS, 0, s>>>(n, x, y, out);
+  else if (op == 2) ew_kernel<K, 2><<<g, EW_THREADS, 0, s>>>(n, x, y, out);
+  else ew_kernel<K, 3><<<g, EW_THREADS, 0, s>>>(n, x, y, out);
   return cudaGetLastError();
 }
 

@@ -36,7 +36,12 @@ struct LuWork {
   unsigned long long *cand_words = nullptr;  // [2][G][LU_CAND_WORDS]
   unsigned long long *row_words = nullptr;   // [2][G][LU_ROW_WORDS]
   unsigned long long *rowj_words = nullptr;  // [2][LU_ROW_WORDS]
-  unsigned *epoch = nullptr;                 // [1] device LU call counter
+  // [0] sequence base of the current LU call, [1] its row count: a call's
+  // words carry base + J + 1 + jj <= base + m + 1; the next call's base
+  // is base + m + 2, and before the 32-bit sequence space would wrap the base
+  // restarts at 0 with every word zeroed (lu_begin_kernel), so no stale
+  // word of an earlier call can ever validate
+  unsigned *epoch = nullptr;
   int32_t *status = nullptr;                 // [0] singular step (or -1)
   int32_t *swap_list = nullptr;  // [2 slots][64 cur | 64 src | count]
   int G = 0;                                 // max CTAs of the panel launch
@@ -97,7 +102,16 @@ struct SolveWork {
   unsigned long long *trace = nullptr;  // MPCORE_TRACE_SOLVE diagnostics
   int64_t trace_len = 0;
   cudaError_t ensure(int64_t rows);
-  unsigned next_seq() { return ++seq; }
+  // a fresh sequence number for one sweep; on 32-bit wrap the words are
+  // zeroed first (stream-ordered), so sequence 0 stays invalid and no
+  // word of a sweep 2^32 calls ago can validate
+  unsigned next_seq(cudaStream_t s) {
+    if (++seq == 0) {
+      cudaMemsetAsync(words, 0, (size_t)2 * LU_MAX_K * cap * sizeof(unsigned long long), s);
+      seq = 1;
+    }
+    return seq;
+  }
 };
 // x <- solve(LU, perm, b): x[i] = b[perm[i]] (the reference's swaps,
 // composed), then forward and back substitution.  b and x must not alias.
@@ -111,7 +125,7 @@ cudaError_t lu_solve_back(int k, int n, MatView LU, double *x, SolveWork &sw,
                           cudaStream_t s);
 
 // panel pieces (exposed for the distributed driver)
-cudaError_t lu_begin(LuWork &ws, cudaStream_t s);
+cudaError_t lu_begin(LuWork &ws, int m, cudaStream_t s);
 // factor panel [J, J+w); its composed row exchanges go to swap-list slot
 cudaError_t lu_panel(int k, int n, MatView A, int J, int w, int32_t *d_swaps,
                      LuWork &ws, int slot, cudaStream_t s);

@@ -102,9 +102,26 @@ __global__ void stamp_kernel(unsigned long long *dst) {
   *dst = t;
 }
 
-__global__ void lu_begin_kernel(unsigned *epoch, int32_t *status) {
-  epoch[0] += 1u;
-  status[0] = -1;
+// One block: advance the sequence base past the previous call's words; on
+// 32-bit wrap restart at 0 and zero every exchange word first.
+__global__ void __launch_bounds__(1024)
+lu_begin_kernel(unsigned *epoch, int32_t *status, unsigned m,
+                unsigned long long *w0, int n0, unsigned long long *w1, int n1,
+                unsigned long long *w2, int n2) {
+  const unsigned long long next =
+      (unsigned long long)epoch[0] + epoch[1] + 2ull;
+  const bool wrap = next + m + 2ull > 0xFFFFFFFFull;
+  __syncthreads();  // every thread has read the old base
+  if (wrap) {
+    for (int i = threadIdx.x; i < n0; i += blockDim.x) w0[i] = 0ull;
+    for (int i = threadIdx.x; i < n1; i += blockDim.x) w1[i] = 0ull;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) w2[i] = 0ull;
+  }
+  if (threadIdx.x == 0) {
+    epoch[0] = wrap ? 0u : (unsigned)next;
+    epoch[1] = m;
+    status[0] = -1;
+  }
 }
 
 // Row exchanges of panel [J, J+w) on every column outside the panel, using
@@ -496,7 +513,7 @@ cudaError_t enqueue_lu(int k, int m, int ncols, MatView A, int32_t *d_swaps,
   cudaError_t e;
   const bool ahead = ws.side != nullptr &&
                      std::getenv("MPCORE_NO_LOOKAHEAD") == nullptr;
-  if ((e = lu_begin(ws, s)) != cudaSuccess) return e;
+  if ((e = lu_begin(ws, m, s)) != cudaSuccess) return e;
   bool panel_pending = false;  // panel J was factored on the side stream
   const int pc = min(m, ncols);  // columns that are pivoted
   for (int J = 0; J < pc; J += nb) {
@@ -587,7 +604,7 @@ cudaError_t LuWork::init(int sms) {
   if ((e = cudaMalloc(&cand_words, cw)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&row_words, rwb)) != cudaSuccess) return e;
   if ((e = cudaMalloc(&rowj_words, jw)) != cudaSuccess) return e;
-  if ((e = cudaMalloc(&epoch, sizeof(unsigned))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&epoch, 2 * sizeof(unsigned))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&status, sizeof(int32_t))) != cudaSuccess) return e;
   if ((e = cudaMalloc(&swap_list, 2 * LU_SWAP_LIST * sizeof(int32_t))) !=
       cudaSuccess)
@@ -596,7 +613,7 @@ cudaError_t LuWork::init(int sms) {
   cudaMemset(cand_words, 0, cw);
   cudaMemset(row_words, 0, rwb);
   cudaMemset(rowj_words, 0, jw);
-  cudaMemset(epoch, 0, sizeof(unsigned));
+  cudaMemset(epoch, 0, 2 * sizeof(unsigned));
   cudaMemset(status, 0xFF, sizeof(int32_t));
   graphs = new GraphCache();
   if (const char *pn = std::getenv("MPCORE_POLL_NS")) poll_ns = std::atoi(pn);
@@ -617,8 +634,11 @@ cudaError_t lu_stamps_enable(unsigned long long *buf) {
   return cudaMemcpyToSymbol(g_lu_stamps, &buf, sizeof(buf));
 }
 
-cudaError_t lu_begin(LuWork &ws, cudaStream_t s) {
-  lu_begin_kernel<<<1, 1, 0, s>>>(ws.epoch, ws.status);
+cudaError_t lu_begin(LuWork &ws, int m, cudaStream_t s) {
+  lu_begin_kernel<<<1, 1024, 0, s>>>(
+      ws.epoch, ws.status, (unsigned)m, ws.cand_words,
+      2 * ws.G * LU_CAND_WORDS, ws.row_words, 2 * ws.G * LU_ROW_WORDS,
+      ws.rowj_words, 2 * LU_ROW_WORDS);
   return cudaGetLastError();
 }
 

@@ -261,6 +261,48 @@ template <int K> MCI void recip(const double *b, double *o) {
   cascade_compress<K + 1, K>(digits, o);
 }
 
+// _sqrt_t (mcfloat.py:324-340): Newton on y ~ 1/sqrt(a) seeded from
+// RN(1 / RN(sqrt(a0))) (both IEEE correctly rounded, as Python's
+// 1.0 / math.sqrt), 2/2/3 steps for DD/TD/QD, then one Heron correction;
+// every step in the reference's operand order.  a0 >= 0 is the caller's
+// check (the reference raises DomainError); an exact zero gives zeros.
+template <int K> MCI void sqrt(const double *a, double *o) {
+  if (a[0] == 0.0) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) o[c] = 0.0;
+    return;
+  }
+  constexpr int STEPS = K == 4 ? 3 : 2;
+  double one[K], y[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) one[c] = y[c] = 0.0;
+  one[0] = 1.0;
+  y[0] = __ddiv_rn(1.0, __dsqrt_rn(a[0]));
+#pragma unroll 1
+  for (int it = 0; it < STEPS; ++it) {
+    double yy[K], ayy[K], r[K], yr[K], h[K], ny[K];
+    mul<K>(y, y, yy);
+    mul<K>(a, yy, ayy);
+#pragma unroll
+    for (int c = 0; c < K; ++c) ayy[c] = -ayy[c];
+    add<K>(one, ayy, r);
+    mul<K>(y, r, yr);
+    mul_scalar<K>(yr, 0.5, h);
+    add<K>(y, h, ny);
+#pragma unroll
+    for (int c = 0; c < K; ++c) y[c] = ny[c];
+  }
+  double s[K], ss[K], e[K], yh[K], ey[K];
+  mul<K>(a, y, s);
+  mul<K>(s, s, ss);
+#pragma unroll
+  for (int c = 0; c < K; ++c) ss[c] = -ss[c];
+  add<K>(a, ss, e);
+  mul_scalar<K>(y, 0.5, yh);
+  mul<K>(e, yh, ey);
+  add<K>(s, ey, o);
+}
+
 // Exact FP64 instruction counts per op (FMA two_prod).
 template <int K> struct Cost;
 template <> struct Cost<2> { static constexpr int madd = 29, mul = 9, add = 20; };

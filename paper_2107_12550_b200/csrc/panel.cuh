@@ -77,7 +77,7 @@ panel_kernel(int n, MatView A, int J, int w, int32_t *__restrict__ swaps,
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     ws.trace[((int64_t)g * 33 + 32) * 8 + 0] = t;
   }
-  const unsigned seq0 = ws.epoch[0] * 65536u + (unsigned)J + 1u;
+  const unsigned seq0 = ws.epoch[0] + (unsigned)J + 1u;  // (LuWork::epoch)
   const int m = n - J;
   const int R = (m + G - 1) / G;
   const int rbeg = J + g * R;

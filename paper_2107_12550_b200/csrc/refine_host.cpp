@@ -531,8 +531,15 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
     }
   }
   const auto t1 = Clock::now();
-  // the factorisation and the first solve (b along the LU on the GPU)
-  if ((st = S.factor_solve(k, n, a_pl.p, b_pl, x_pl, err))) return st;
+  // the factorisation and the first solve (b along the LU on the GPU);
+  // MPCORE_REFINE_SPLIT_FACTOR=1 takes factor() + solve() instead (tests:
+  // both give the same bits)
+  if (std::getenv("MPCORE_REFINE_SPLIT_FACTOR") != nullptr) {
+    if ((st = S.factor(k, n, a_pl.p, err))) return st;
+    if ((st = S.solve(b_pl, x_pl, err))) return st;
+  } else if ((st = S.factor_solve(k, n, a_pl.p, b_pl, x_pl, err))) {
+    return st;
+  }
   const auto t2 = Clock::now();
   plog.mark("factor + first solve");
   double t_solve = 0, t_res = 0;

@@ -405,10 +405,10 @@ cudaError_t solve_k(int n, MatView LU, const int32_t *perm, const double *b,
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   u64 *tf = sw.trace, *tb = sw.trace ? sw.trace + (int64_t)8 * nblk : nullptr;
   e = launch_coop(fk, coop_grid(fk, smem, nblk), smem, s, n, LU, x, sw.words,
-                  sw.next_seq(), tf);
+                  sw.next_seq(s), tf);
   if (e != cudaSuccess) return e;
   return launch_coop(bk, coop_grid(bk, smem, nblk), smem, s, n, LU, x,
-                     sw.words, sw.next_seq(), tb);
+                     sw.words, sw.next_seq(s), tb);
 }
 
 template <int K>
@@ -429,7 +429,7 @@ cudaError_t back_k(int n, MatView LU, double *x, SolveWork &sw,
   if ((e = sw.ensure(n)) != cudaSuccess) return e;
   u64 *tb = sw.trace ? sw.trace + (int64_t)8 * nblk : nullptr;
   return launch_coop(bk, coop_grid(bk, smem, nblk), smem, s, n, LU, x,
-                     sw.words, sw.next_seq(), tb);
+                     sw.words, sw.next_seq(s), tb);
 }
 
 }  // namespace

@@ -24,7 +24,7 @@ from .errors import (ArithmeticOverflowError, DimensionError,
 RND = "n"
 FZERO = L.fzero
 
-__all__ = ["LF", "PrecisionContext", "BfDomain", "parse_decimal",
+__all__ = ["BigFloat", "LF", "PrecisionContext", "BfDomain", "parse_decimal",
            "format_decimal", "convert_vector", "convert_matrix"]
 
 
@@ -49,11 +49,151 @@ class PrecisionContext:
         return hash(("PrecisionContext", self.p))
 
 
-class LF:
-    """One long-precision value: raw mpf tuple + the precision it was last
-    rounded to (BigFloat.prec bookkeeping, bigfloat.py:74-90)."""
+class BigFloat:
+    """One long-precision value (the reference's BigFloat, bigfloat.py:73-158):
+    value = sign * man * 2**exp, prec = the precision it was last rounded to
+    (bookkeeping only: comparisons and hashing ignore it).
+
+    Stored as mpmath's raw mpf tuple ``v`` (odd mantissa; the reference's
+    _strip form), so every operation of this module is one correctly
+    rounded mpmath call.  ``BigFloat(sign, man, exp, prec)`` is the
+    reference constructor; the module's own results are built through
+    ``LF(v, prec)`` (a subclass: every LF is a BigFloat).
+    """
 
     __slots__ = ("v", "prec")
+
+    def __init__(self, sign, man, exp, prec):
+        sign, man, exp = int(sign), int(man), int(exp)
+        if sign == 0 or man == 0:
+            self.v = FZERO
+        else:
+            if man < 0:
+                man, sign = -man, -sign
+            tz = (man & -man).bit_length() - 1
+            man, exp = man >> tz, exp + tz
+            self.v = (1 if sign < 0 else 0, man, exp, man.bit_length())
+        self.prec = int(prec)
+
+    def to_float(self):
+        """Nearest binary64 (bf_to_binary64, bigfloat.py:375-387)."""
+        r = L.to_float(self.v, rnd=RND)
+        if math.isinf(r):
+            raise ArithmeticOverflowError("value does not fit in binary64")
+        return r
+
+    def to_components(self, k):
+        """Peel k rounded binary64 heads (bf_to_multicomp, 419-432)."""
+        comps = []
+        r = self.v
+        for _ in range(k):
+            c = L.to_float(r, rnd=RND)
+            if math.isinf(c):
+                raise ArithmeticOverflowError("value does not fit in binary64")
+            comps.append(c)
+            if c != 0.0:
+                r = L.mpf_sub(r, L.from_float(c))
+        return tuple(comps)
+
+    def round(self, p):
+        if self.v == FZERO:
+            return LF(FZERO, p)
+        if self.v[3] <= p:
+            return self if self.prec == p else LF(self.v, p)
+        return LF(L.mpf_pos(self.v, p, RND), p)
+
+    # the reference's attribute surface (sign in {-1, 0, 1}, man >= 0)
+    @property
+    def sign(self):
+        if not self.v[1]:
+            return 0
+        return -1 if self.v[0] else 1
+
+    @property
+    def man(self):
+        return int(self.v[1])
+
+    @property
+    def exp(self):
+        return int(self.v[2]) if self.v[1] else 0
+
+    def is_zero(self):
+        return not self.v[1]
+
+    # operators round at the larger operand precision (BigFloat._ctx)
+    def _p(self, other):
+        return max(self.prec, other.prec)
+
+    def __add__(self, other):
+        if not isinstance(other, BigFloat):
+            return NotImplemented
+        return lf_add(self, other, self._p(other))
+
+    def __sub__(self, other):
+        if not isinstance(other, BigFloat):
+            return NotImplemented
+        return lf_sub(self, other, self._p(other))
+
+    def __mul__(self, other):
+        if not isinstance(other, BigFloat):
+            return NotImplemented
+        return lf_mul(self, other, self._p(other))
+
+    def __truediv__(self, other):
+        if not isinstance(other, BigFloat):
+            return NotImplemented
+        return lf_div(self, other, self._p(other))
+
+    def __neg__(self):
+        return lf_neg(self)
+
+    def __abs__(self):
+        return lf_abs(self)
+
+    def __float__(self):
+        return self.to_float()
+
+    def __eq__(self, other):
+        if not isinstance(other, BigFloat):
+            return NotImplemented
+        return L.mpf_cmp(self.v, other.v) == 0
+
+    def __ne__(self, other):
+        eq = self.__eq__(other)
+        return eq if eq is NotImplemented else not eq
+
+    def __lt__(self, other):
+        if not isinstance(other, BigFloat):
+            return NotImplemented
+        return L.mpf_cmp(self.v, other.v) < 0
+
+    def __le__(self, other):
+        if not isinstance(other, BigFloat):
+            return NotImplemented
+        return L.mpf_cmp(self.v, other.v) <= 0
+
+    def __gt__(self, other):
+        if not isinstance(other, BigFloat):
+            return NotImplemented
+        return L.mpf_cmp(self.v, other.v) > 0
+
+    def __ge__(self, other):
+        if not isinstance(other, BigFloat):
+            return NotImplemented
+        return L.mpf_cmp(self.v, other.v) >= 0
+
+    def __hash__(self):
+        return hash(self.v)
+
+    def __repr__(self):
+        return "BigFloat(%s, prec=%d)" % (format_hex(self), self.prec)
+
+
+class LF(BigFloat):
+    """A BigFloat built from a raw mpf tuple (this module's internal
+    constructor): ``LF(v, prec)``."""
+
+    __slots__ = ()
 
     def __init__(self, v, prec):
         self.v = v
@@ -86,54 +226,6 @@ class LF:
         if prec is None:
             return cls(acc, max(acc[3], 53))
         return cls(L.mpf_pos(acc, prec, RND), prec)
-
-    def to_float(self):
-        """Nearest binary64 (bf_to_binary64, bigfloat.py:375-387)."""
-        r = L.to_float(self.v, rnd=RND)
-        if math.isinf(r):
-            raise ArithmeticOverflowError("value does not fit in binary64")
-        return r
-
-    def to_components(self, k):
-        """Peel k rounded binary64 heads (bf_to_multicomp, 419-432)."""
-        comps = []
-        r = self.v
-        for _ in range(k):
-            c = L.to_float(r, rnd=RND)
-            if math.isinf(c):
-                raise ArithmeticOverflowError("value does not fit in binary64")
-            comps.append(c)
-            if c != 0.0:
-                r = L.mpf_sub(r, L.from_float(c))
-        return tuple(comps)
-
-    def round(self, p):
-        if self.v == FZERO:
-            return LF(FZERO, p)
-        if self.v[3] <= p:
-            return self if self.prec == p else LF(self.v, p)
-        return LF(L.mpf_pos(self.v, p, RND), p)
-
-    @property
-    def sign(self):
-        if not self.v[1]:
-            return 0
-        return -1 if self.v[0] else 1
-
-    def is_zero(self):
-        return not self.v[1]
-
-    def __repr__(self):
-        return "LF(%s, prec=%d)" % (format_decimal(self, 20), self.prec)
-
-    def __float__(self):
-        return self.to_float()
-
-    def __eq__(self, other):
-        return isinstance(other, LF) and L.mpf_cmp(self.v, other.v) == 0
-
-    def __hash__(self):
-        return hash(self.v)
 
 
 def lf_add(a, b, p):

@@ -16,7 +16,7 @@ from .errors import ArithmeticOverflowError, DivideByZeroError, DomainError
 from .linalg import PrecisionTag, DD, TD, QD  # noqa: F401
 
 __all__ = ["MultiComp", "PrecisionTag", "mc_add", "mc_sub", "mc_mul",
-           "mc_div", "mc_neg", "mc_abs", "mc_cmp", "from_binary64",
+           "mc_div", "mc_sqrt", "mc_neg", "mc_abs", "mc_cmp", "from_binary64",
            "to_binary64"]
 
 
@@ -144,7 +144,8 @@ def _same_width(a, b):
 def _device_op(op, a, b):
     k = a.k
     x = np.array(a.components, dtype=np.float64).reshape(k, 1)
-    y = np.array(b.components, dtype=np.float64).reshape(k, 1)
+    y = np.array((b if b is not None else a).components,
+                 dtype=np.float64).reshape(k, 1)
     hx, hy, ho = (nat.Handle(nat.new_vector(k, 1)) for _ in range(3))
     nat.set_planes(hx.h, x)
     nat.set_planes(hy.h, y)
@@ -178,6 +179,15 @@ def mc_div(a, b):
     if b.components[0] == 0.0:
         raise DivideByZeroError("division by zero")
     return _device_op(2, a, b)
+
+
+def mc_sqrt(a):
+    """Square root (mcfloat.py:596-601, _sqrt_t 324-340): Newton on
+    1/sqrt(a) then one Heron correction, on the device (elementwise op 3).
+    Raises DomainError for a negative value; sqrt(0) is exactly zero."""
+    if a.components[0] < 0.0:
+        raise DomainError("square root of a negative value")
+    return _device_op(3, a, None)
 
 
 def mc_neg(a):
