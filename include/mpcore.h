@@ -236,6 +236,39 @@ int32_t mpcore_dev_generate_cyclic(int32_t k, uint64_t base, int64_t ld,
                                    int32_t world, int32_t rank, int32_t slot,
                                    int64_t system_n, uint64_t seed);
 
+/* ---- extensions: the distributed LU + solve (BASELINE config 4) --------
+ * One process per GPU.  Rank 0 draws an NCCL unique id (128 bytes) and the
+ * host shares it over its own channel (torch.distributed, MPI, a file);
+ * every rank then creates its communicator.  libnccl.so.2 is loaded on
+ * first use (the copy already in the process if any, else MPCORE_NCCL_LIB,
+ * else the loader's); without it these calls return 6. */
+int32_t mpcore_dist_unique_id(uint8_t *out, int32_t cap);
+int32_t mpcore_dist_comm_init(int32_t world, int32_t rank, const uint8_t *id,
+                              int32_t len, uint64_t *comm_out);
+int32_t mpcore_dist_comm_destroy(uint64_t comm);
+/* Factor A (n x n, column-block-cyclic: block b of nb columns on rank
+ * b % world) with partial pivoting and solve A x = b, stream-ordered on the
+ * device (linalg.py:422-538 per element; pivots, factors and x bitwise the
+ * one-GPU result).  comm = a communicator (this process serves one rank,
+ * nlocal = 1) or 0 (this process serves every rank of the world on its
+ * device: nlocal = world, broadcasts become device copies).  Per served
+ * rank i: ranks[i], the local matrix at bases[i] (lds[i], planes[i]) with
+ * cols[i] = its local column count + 1, the last column holding b on
+ * entry (y = L^-1 P b on exit), and xs[i] (device, k*n planar) for x.
+ * The work starts after `stream`'s queued work (0: the library stream) and
+ * that stream waits for its end.  swaps_out (host, n) = PivotRecord.swaps;
+ * phase_ms (6, optional, one served rank only): total, tall-block factor +
+ * pack, broadcasts, exchanges + U12, trailing update, back substitution;
+ * launches (optional): kernels + collectives enqueued.  3 = singular. */
+int32_t mpcore_dist_lu_solve(uint64_t comm, int32_t k, int32_t n, int32_t nb,
+                             int32_t world, int32_t nlocal,
+                             const int32_t *ranks, const uint64_t *bases,
+                             const int64_t *lds, const int64_t *planes,
+                             const int32_t *cols, const uint64_t *xs,
+                             uint64_t stream, int32_t *swaps_out,
+                             int32_t *singular_step, double *phase_ms,
+                             int64_t *launches);
+
 /* ---- extensions: device, diagnostics, profiling ------------------------ */
 
 /* select the CUDA device for this process (before any other call) */

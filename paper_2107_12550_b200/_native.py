@@ -114,6 +114,17 @@ _PROTOS = {
     "mpcore_dev_generate_cyclic": (_i32, [_i32, _u64, _i64, _i64, _i32, _i32,
                                           _i32, _i32, _i32, _i32, _i64,
                                           _u64]),
+    # the native distributed LU + solve (dist.cu; BASELINE config 4)
+    "mpcore_dist_unique_id": (_i32, [ctypes.c_char_p, _i32]),
+    "mpcore_dist_comm_init": (_i32, [_i32, _i32, ctypes.c_char_p, _i32,
+                                     ctypes.POINTER(_u64)]),
+    "mpcore_dist_comm_destroy": (_i32, [_u64]),
+    "mpcore_dist_lu_solve": (_i32, [_u64, _i32, _i32, _i32, _i32, _i32, _ip,
+                                    ctypes.POINTER(_u64),
+                                    ctypes.POINTER(_i64),
+                                    ctypes.POINTER(_i64), _ip,
+                                    ctypes.POINTER(_u64), _u64, _ip, _ip,
+                                    _dp, ctypes.POINTER(_i64)]),
 }
 
 # The 16 symbols of the reference ABI (build_lib.py:31-57).

@@ -27,6 +27,8 @@
 #include "longfloat.cuh"
 #include "refine_host.h"
 #include "testsys.h"
+#include "dist.h"
+#include <set>
 
 namespace {
 
@@ -1893,6 +1895,89 @@ int32_t mpcore_dev_generate_cyclic(int32_t k, uint64_t base, int64_t ld,
                                        system_n, seed, device().stream);
   if (e != cudaSuccess) return cuda_fail(e, "generate_cyclic");
   return finish("generate_cyclic");
+}
+
+
+// ------------------------------------------------ distributed LU ----
+// NCCL bootstrap (unique id on one rank, shared by the host's own channel,
+// then one communicator per rank) and the native distributed driver
+// (dist.cu).  Communicator handles are opaque and checked against the
+// live set.
+static std::set<uint64_t> &live_comms() {
+  static std::set<uint64_t> s;
+  return s;
+}
+
+int32_t mpcore_dist_unique_id(uint8_t *out, int32_t cap) {
+  if (!out || cap < 128) return MPCORE_BAD_DIMENSION;
+  std::string err;
+  if (mpk::nccl_unique_id(out, err)) return fail(MPCORE_INTERNAL, err);
+  return MPCORE_OK;
+}
+
+int32_t mpcore_dist_comm_init(int32_t world, int32_t rank, const uint8_t *id,
+                              int32_t len, uint64_t *comm_out) {
+  if (!comm_out) return MPCORE_BAD_DIMENSION;
+  *comm_out = 0;
+  if (!id || len != 128 || world < 1 || rank < 0 || rank >= world)
+    return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  std::string err;
+  void *c = mpk::nccl_comm_init(world, rank, id, err);
+  if (!c) return fail(MPCORE_INTERNAL, err);
+  *comm_out = reinterpret_cast<uint64_t>(c);
+  live_comms().insert(*comm_out);
+  return MPCORE_OK;
+}
+
+int32_t mpcore_dist_comm_destroy(uint64_t comm) {
+  DevLock L;
+  if (!live_comms().erase(comm)) return MPCORE_BAD_HANDLE;
+  mpk::nccl_comm_destroy(reinterpret_cast<void *>(comm));
+  return MPCORE_OK;
+}
+
+int32_t mpcore_dist_lu_solve(uint64_t comm, int32_t k, int32_t n, int32_t nb,
+                             int32_t world, int32_t nlocal,
+                             const int32_t *ranks, const uint64_t *bases,
+                             const int64_t *lds, const int64_t *planes,
+                             const int32_t *cols, const uint64_t *xs,
+                             uint64_t stream, int32_t *swaps_out,
+                             int32_t *singular_step, double *phase_ms,
+                             int64_t *launches) {
+  if (singular_step) *singular_step = -1;
+  if (k < 2 || k > 4 || n < 1 || nb < 1 || world < 1 || nlocal < 1 ||
+      !ranks || !bases || !lds || !planes || !cols || !xs || !swaps_out)
+    return MPCORE_BAD_DIMENSION;
+  std::vector<mpk::DistRankView> views(nlocal);
+  for (int i = 0; i < nlocal; ++i) {
+    if (ranks[i] < 0 || ranks[i] >= world || !bases[i] || !xs[i])
+      return MPCORE_BAD_DIMENSION;
+    views[i].rank = ranks[i];
+    views[i].A = mv(bases[i], lds[i], planes[i]);
+    views[i].cols = cols[i];
+    views[i].x = reinterpret_cast<double *>(xs[i]);
+  }
+  DevLock L;
+  if (L.st) return L.st;
+  if (comm && !live_comms().count(comm)) return MPCORE_BAD_HANDLE;
+  Device &D = device();
+  cudaStream_t caller =
+      stream ? reinterpret_cast<cudaStream_t>(stream) : D.stream;
+  std::vector<int32_t> sw;
+  std::string err;
+  int32_t step = -1;
+  int st = mpk::dist_lu_solve(reinterpret_cast<void *>(comm), k, n, nb, world,
+                              views, D.ws, D.sw, caller, sw, &step, phase_ms,
+                              launches, err);
+  if (singular_step) *singular_step = step;
+  if (st == 0 || st == MPCORE_SINGULAR)
+    std::memcpy(swaps_out, sw.data(), (size_t)n * sizeof(int32_t));
+  if (st == 2) return fail(MPCORE_BAD_DIMENSION, err);
+  if (st == 3) return fail(MPCORE_SINGULAR, err);
+  if (st) return fail(MPCORE_INTERNAL, err);
+  return MPCORE_OK;
 }
 
 }  // extern "C"

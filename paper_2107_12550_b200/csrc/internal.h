@@ -93,6 +93,11 @@ cudaError_t gemm(int k, bool neg_a, bool zero_init, int M, int N, int KK,
 // singular step or -1.  nb = panel width (<= 32).
 cudaError_t lu_factor(int k, int m, int ncols, MatView A, int32_t *d_swaps,
                       int nb, LuWork &w, int32_t *sing_step, cudaStream_t s);
+// the same, stream-ordered only: no host synchronisation; the singular step
+// (or -1) stays in w.status[0] on the device
+cudaError_t lu_factor_async(int k, int m, int ncols, MatView A,
+                            int32_t *d_swaps, int nb, LuWork &w,
+                            cudaStream_t s);
 // Scratch of the pipelined triangular solves: every final x_i is published
 // as 2K self-validating words (32-bit payload | 32-bit sequence), [2K][rows].
 struct SolveWork {

@@ -705,8 +705,9 @@ cudaError_t lu_trsm(int k, MatView L11, MatView U12, int w, int ncols,
   return e;
 }
 
-cudaError_t lu_factor(int k, int m, int ncols, MatView A, int32_t *d_swaps,
-                      int nb, LuWork &ws, int32_t *sing_step, cudaStream_t s) {
+cudaError_t lu_factor_async(int k, int m, int ncols, MatView A,
+                            int32_t *d_swaps, int nb, LuWork &ws,
+                            cudaStream_t s) {
   cudaError_t e;
   if (nb > LU_MAX_W) nb = LU_MAX_W;
   if (nb < 1) nb = 1;
@@ -747,6 +748,13 @@ cudaError_t lu_factor(int k, int m, int ncols, MatView A, int32_t *d_swaps,
     }
     if ((e = cudaGraphLaunch(exec, s)) != cudaSuccess) return e;
   }
+  return cudaSuccess;
+}
+
+cudaError_t lu_factor(int k, int m, int ncols, MatView A, int32_t *d_swaps,
+                      int nb, LuWork &ws, int32_t *sing_step, cudaStream_t s) {
+  cudaError_t e = lu_factor_async(k, m, ncols, A, d_swaps, nb, ws, s);
+  if (e != cudaSuccess) return e;
   e = cudaMemcpyAsync(sing_step, ws.status, sizeof(int32_t),
                       cudaMemcpyDeviceToHost, s);
   if (e != cudaSuccess) return e;

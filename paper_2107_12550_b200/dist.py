@@ -23,13 +23,15 @@ with world_size 2.  `local_ranks` lets one process act for several ranks
 (one GPU emulating G ranks serially, broadcast = sharing the buffer).
 """
 
+import ctypes
+
 import numpy as np
 
 from . import _native as nat
 from .errors import SingularMatrixError
 
 __all__ = ["Layout", "DeviceBackend", "TorchComm", "LocalComm",
-           "dist_lu_factor"]
+           "dist_lu_factor", "NcclComm", "dist_lu_solve", "DIST_PHASES"]
 
 
 class Layout:
@@ -345,3 +347,84 @@ def _split_out(ranges, a0, m0):
         if b > a0 + m0:
             out.append((a0 + m0, b - a0 - m0))
     return out
+
+
+# ------------------------------------------------------------------------
+# The native driver (libmpcore dist.cu): the same protocol, device-ordered.
+# The functions above are its executable specification on any backend
+# (tests/test_dist_gloo.py runs them on CPU over gloo); the product path
+# for BASELINE config 4 is dist_lu_solve below: one C-ABI call per solve,
+# pivots on the device, the panel loop, broadcasts (live rows only),
+# look-ahead and the column-cyclic back substitution all enqueued by the
+# library on its own streams, ordered after / before the caller's stream.
+
+DIST_PHASES = ("total", "factor", "bcast", "exch_trsm", "update", "back")
+
+
+class NcclComm:
+    """libmpcore's own NCCL communicator for this rank.  The unique id is
+    drawn on rank 0 and shared through the caller's torch.distributed
+    group (any backend; one small object broadcast at setup)."""
+
+    def __init__(self, world, rank, group=None):
+        import torch.distributed as dist
+        L = nat.lib()
+        obj = [None]
+        if rank == 0:
+            buf = ctypes.create_string_buffer(128)
+            nat.check(L.mpcore_dist_unique_id(buf, 128), "dist_unique_id")
+            obj[0] = buf.raw
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        h = nat._u64()
+        nat.check(L.mpcore_dist_comm_init(world, rank, obj[0], 128,
+                                          ctypes.byref(h)), "dist_comm_init")
+        self.handle, self.world, self.rank = h.value, world, rank
+
+    def close(self):
+        if self.handle:
+            nat.lib().mpcore_dist_comm_destroy(self.handle)
+            self.handle = 0
+
+
+def dist_lu_solve(layout, local, xs, k, comm=None, stream=0, phases=False):
+    """Factor the distributed matrix and solve (one library call).
+
+    local: {rank: device tensor (k, n, local_cols + 1)}, the last column
+    holding b (every rank) -- y = L^-1 P b on exit; xs: {rank: device tensor
+    (k, n)} receiving x.  comm: an NcclComm (this process serves its one
+    rank) or None (every rank of the layout served here on one device).
+    stream: the CUDA stream (int handle) the work is ordered after and that
+    waits for it (0: the library stream).  Returns (swaps, phase_ms or
+    None, launches); raises SingularMatrixError(step) like lu_factor_pp."""
+    ranks = sorted(local)
+    R = len(ranks)
+    arr = lambda t, vals: (t * R)(*vals)  # noqa: E731
+    for r in ranks:
+        M = local[r]
+        assert M.shape[0] == k and M.shape[1] == layout.n
+        assert M.shape[2] == layout.local_cols(r) + 1 and M.is_contiguous()
+    rk = arr(ctypes.c_int32, ranks)
+    bases = arr(nat._u64, [local[r].data_ptr() for r in ranks])
+    lds = arr(ctypes.c_int64, [local[r].shape[2] for r in ranks])
+    planes = arr(ctypes.c_int64, [local[r].shape[1] * local[r].shape[2]
+                                  for r in ranks])
+    cols = arr(ctypes.c_int32, [local[r].shape[2] for r in ranks])
+    xp = arr(nat._u64, [xs[r].data_ptr() for r in ranks])
+    swaps = np.zeros(layout.n, dtype=np.int32)
+    step = nat._i32(-1)
+    ph = (ctypes.c_double * len(DIST_PHASES))() if phases else None
+    nl = ctypes.c_int64(0)
+    st = nat.lib().mpcore_dist_lu_solve(
+        comm.handle if comm is not None else 0, k, layout.n, layout.nb,
+        layout.world, R, rk, bases, lds, planes, cols, xp, int(stream),
+        nat.iptr(swaps), ctypes.byref(step),
+        ctypes.cast(ph, nat._dp) if ph is not None else None,
+        ctypes.byref(nl))
+    if st == nat.SINGULAR:
+        raise SingularMatrixError(
+            "no nonzero pivot at elimination step %d" % step.value,
+            step=step.value)
+    nat.check(st, "dist_lu_solve")
+    return (swaps, dict(zip(DIST_PHASES, list(ph))) if ph is not None
+            else None, nl.value)
