@@ -10,8 +10,14 @@ the same recipe, b = A*x_true in TD on the device).  A step = restore A
     python bench.py [--gpus N] [--steps K] [--warmup W] [--k 3] [--dim 2048]
     python bench.py --impl reference ...   (CPU oracle port, all host threads)
 
-Multi-GPU (torchrun, one rank per GPU): independent replicas of the same
-system per rank ("replicas only" for configs 0-3), barrier + max over ranks.
+    python bench.py --config {1,3,4}       (GEMM, TD-mpmath IR, distributed)
+
+Multi-GPU (torchrun, one rank per GPU): without --config, BASELINE config 4
+-- ONE DD n = 32768 system, column-block-cyclic over the ranks through the
+native distributed driver (strong scaling; `--config 4` at N = 1 is the
+same code with a one-rank world, the curve's first point).  Configs 1-3
+are single-GPU workloads ("replicas only" under torchrun).  Barrier + max
+over ranks of the device time.
 """
 
 import argparse
@@ -167,7 +173,7 @@ def max_over_ranks(pg, v):
     return float(t.item())
 
 
-def cpu_baseline(k, n_sample, threads=None):
+def cpu_baseline(k, n_sample, threads=None, seed=SEED):
     """Oracle port (C++/AVX2/OpenMP restatement of the reference lane
     path) on a bounded sample: LU + solve of the same recipe at n_sample."""
     import oracle
@@ -181,8 +187,8 @@ def cpu_baseline(k, n_sample, threads=None):
             threads = os.cpu_count() or 1
     oracle.set_threads(threads)
     cores = oracle.num_threads()
-    A = gen.planes(k, (n_sample, n_sample), 0, n_sample, SEED)
-    x = gen.planes(k, (n_sample,), 2, n_sample, SEED)
+    A = gen.planes(k, (n_sample, n_sample), 0, n_sample, seed)
+    x = gen.planes(k, (n_sample,), 2, n_sample, seed)
     b = oracle.matvec(A, x)
     t0 = time.perf_counter()
     lu, sw = oracle.lu(A)
@@ -196,29 +202,113 @@ def cpu_baseline(k, n_sample, threads=None):
                        "AVX2 + OpenMP over rows" % (NAMES[k], n_sample, dt))
 
 
+def config_dict(args, world):
+    """The workload's config object -- the same dict on both arms."""
+    k, n = args.k, args.n
+    if args.config == 1:
+        return {"workload": "config1: %s GEMM n=%d" % (NAMES[k], n),
+                "n": n, "k": k, "parallelism": "replicas x%d" % world,
+                "l2": "A, B, C = 3 x %d MB (> L2)" % (k * n * n * 8 >> 20)}
+    if args.config == 3:
+        return {"workload": "config3: TD-mpmath IR n=%d kappa=1e30" % n,
+                "n": n, "long_bits": 512, "rtol": "1e-100", "atol": "0",
+                "maxtimes": 20, "parallelism": "replicas x%d" % world}
+    if args.config == 4:
+        return {"workload": "config4: distributed %s LU+PP+solve n=%d"
+                % (NAMES[k], n), "n": n, "k": k, "nb": args.dist_nb,
+                "parallelism": "column-block-cyclic x%d (one process per "
+                "GPU), NCCL panel + pivot broadcast, column-cyclic back "
+                "substitution" % world,
+                "l2": "A restored from a pristine copy each step (>> L2)"}
+    return {"workload": "config2: %s LU+PP+solve n=%d" % (NAMES[k], n),
+            "n": n, "k": k, "nb": args.nb or 32,
+            "l2": "A restored by a 2x%d MB D2D copy each step (> L2)"
+                  % (k * n * n * 8 // 2 ** 20),
+            "parallelism": "replicas x%d" % world}
+
+
 def run_reference(args):
+    """The reference arm: the reference's CPU path for the same workload,
+    timed on this box's host cores -- the oracle port (C++ restatement of
+    the reference lane path, AVX2 + OpenMP over rows; the pure-Python
+    reference does not exist on the GPU box and takes ~25 min per config-2
+    solve).  Each step is a bounded sample of the workload: the full
+    config-2 LU + solve; for config 1 an n = 1024 GEMM; for config 3 the
+    short side (TD LU + the solves) of the refinement; for config 4 a DD
+    n = 4096 LU + solve whose rate stands for n = 32768 (time x 512).
+    Rank 0 only under torchrun."""
     world, rank, local, pg = dist_setup(args)
     if rank != 0:
         return
+    import oracle
+    from oracle import gen
     k, n = args.k, args.n
-    n_sample = args.cpu_n or n
+    try:
+        threads = len(os.sched_getaffinity(0))
+    except AttributeError:
+        threads = os.cpu_count() or 1
+    oracle.set_threads(threads)
     res = []
     for i in range(args.warmup + args.steps):
-        r = cpu_baseline(k, n_sample)
+        if args.config == 1:
+            ns = args.cpu_n or 1024
+            A = gen.planes(k, (ns, ns), 0, ns, 210712551)
+            B = gen.planes(k, (ns, ns), 1, ns, 210712551)
+            t0 = time.perf_counter()
+            oracle.gemm(A, B)
+            dt = time.perf_counter() - t0
+            r = dict(value=2.0 * ns ** 3 / dt / 1e9, seconds=dt,
+                     sample="%s GEMM n=%d of the config-1 recipe" %
+                            (NAMES[k], ns))
+        elif args.config == 3:
+            from paper_2107_12550_b200.refine import CONFIG3_SEED  # noqa
+            A = gen.planes(3, (n, n), 0, n, CONFIG3_SEED)
+            b = gen.planes(3, (n,), 2, n, CONFIG3_SEED)
+            t0 = time.perf_counter()
+            lu, sw = oracle.lu(A)
+            for _ in range(4):       # the first solve + 3 corrections
+                oracle.solve(lu, sw, b)
+            dt = time.perf_counter() - t0
+            r = dict(value=dt, seconds=dt,
+                     sample="short side of the config-3 refinement only "
+                            "(TD LU n=%d + 4 solves; the reference's "
+                            "512-bit residual loop is pure Python and not "
+                            "ported): a lower bound of its CPU time" % n)
+        else:
+            ns = args.cpu_n or (4096 if args.config == 4 else n)
+            seed = 210712550 + (4 if args.config == 4 else 2)
+            r = cpu_baseline(k, ns, threads, seed=seed)
+            if args.config == 4:
+                r["sample"] += ("; rate at n=%d stands for n=%d "
+                                "(time x (n/%d)^3)" % (ns, n, ns))
         if i >= args.warmup:
             res.append(r)
     v = statistics.median([r["value"] for r in res])
-    ms = statistics.median([r["seconds"] for r in res]) * 1e3
+    sec = statistics.median([r["seconds"] for r in res])
+    if args.config == 3:
+        metric, unit, hib = "TD-mpmath IR time-to-rtol (s)", "s", False
+        ms = sec * 1e3
+    elif args.config == 1:
+        metric, unit, hib = "%s GEMM eff. GFLOP/s (2n^3/s)" % NAMES[k], \
+            "GFLOP/s", True
+        ms = sec * 1e3
+    else:
+        metric, unit, hib = ("%s LU+solve eff. GFLOP/s ((2/3)n^3/s)"
+                             % NAMES[k]), "GFLOP/s", True
+        ms = (2.0 / 3.0) * n ** 3 / (v * 1e9) * 1e3
     line = {
-        "impl": "reference", "metric": "%s LU+solve eff. GFLOP/s ((2/3)n^3/s)"
-        % NAMES[k], "value": v, "unit": "GFLOP/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64x%d" % k, "data": "synthetic",
-        "config": {"workload": "config2: %s LU+PP+solve n=%d" % (NAMES[k], n),
-                   "sample_n": n_sample},
-        "cpu_baseline": dict(res[-1], value=v),
-        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+        "impl": "reference", "metric": metric, "value": v, "unit": unit,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": hib,
+        "scaling": "strong" if args.config == 4 else "weak",
+        "vs_baseline": None, "dtype": "f64x%d" % k,
+        "data": "synthetic (the same seeded recipe)",
+        "config": config_dict(args, world),
+        "cpu_baseline": {"value": v, "unit": unit, "cores": threads,
+                         "kind": "port", "seconds": sec,
+                         "sample": res[-1]["sample"] + " (median of %d)"
+                         % len(res)},
+        "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -312,21 +402,24 @@ def run_ours(args):
         nat.set_planes_async(Es[slot].handle, hA.array)
         nat.set_planes_async(ebs[slot].handle, hb.array)
 
-    def e2e_step(i):
-        upload((i + 1) % 2)                       # the next step's inputs
-        device_solve_system(Es[i % 2], ebs[i % 2], ex, nb)
-        ex.download(hx.array)
-
+    # warm-up pass, then K timed steps: the first timed step's upload is
+    # inside the timed region too, the last step queues none, so the
+    # region holds exactly K uploads, K solves and K downloads
     upload(0)
-    e2e_step(0)                                   # warm-up (slot 1 queued)
+    device_solve_system(Es[0], ebs[0], ex, nb)
+    ex.download(hx.array)
     barrier(pg)
     nat.sync()
-    e_steps = max(1, min(args.steps, 5))
+    e_steps = args.steps
     timer.start()
+    upload(1)
     for i in range(1, e_steps + 1):
-        e2e_step(i)
-    e2e_ms = max_over_ranks(pg, timer.stop() / e_steps)
+        if i < e_steps:
+            upload((i + 1) % 2)                   # the next step's inputs
+        device_solve_system(Es[i % 2], ebs[i % 2], ex, nb)
+        ex.download(hx.array)                     # synchronous D2H of x
     nat.sync()
+    e2e_ms = max_over_ranks(pg, timer.stop() / e_steps)
     assert hx.array.tobytes() == x.download().tobytes()
 
     if rank != 0:
@@ -355,11 +448,7 @@ def run_ours(args):
         "dtype": "f64x%d (%s, bit-exact EFT arithmetic)" % (k, NAMES[k]),
         "data": "synthetic (seeded splitmix64 recipe, SURVEY 8d; seed %d)"
                 % seed,
-        "config": {"workload": "config2: %s LU+PP+solve n=%d" % (NAMES[k], n),
-                   "n": n, "k": k, "nb": nb or 32,
-                   "l2": "A restored by a 2x%d MB D2D copy each step (> L2)"
-                         % (k * n * n * 8 // 2 ** 20),
-                   "parallelism": "replicas x%d" % world},
+        "config": config_dict(args, world),
         "e2e": {"value": world * flops / (e2e_ms * 1e-3) / 1e9,
                 "unit": "GFLOP/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": (k * n * n + k * n) * 8,
@@ -369,7 +458,8 @@ def run_ours(args):
                         "stream, overlapping this step's solve) + "
                         "solve_system (LU with b as an extra column + back "
                         "substitution; = lu_factor + lu_solve bit for bit) + "
-                        "get_planes(x)"},
+                        "get_planes(x); K uploads, K solves, K downloads "
+                        "between the events"},
         "roofline": {
             "bound": "fp64",
             "kernel": "trailing update, wide launches (gemm_kernel NEG_A; "
@@ -423,85 +513,25 @@ def traffic_bytes(k, n):
     return d["dram_bytes"] if (d.get("k"), d.get("n")) == (k, n) else None
 
 
-def run_single_config4(args):
-    """BASELINE config 4 at one GPU: the same seeded system (one rank's
-    column-block-cyclic layout is the plain layout) through the one-call
-    LU + solve ([A | b] factored together, back substitution); bitwise the
-    distributed protocol's result (tests/test_gpu_dist.py)."""
-    from paper_2107_12550_b200 import _native as nat
-    from paper_2107_12550_b200.linalg import DeviceMatrix, DeviceVector
-    k, n = args.k, args.n
-    seed = 210712550 + 4
-    L = nat.lib()
-    A0 = DeviceMatrix(k, n, n)
-    A0.generate(0, n, seed)
-    ones = np.zeros((k, n))
-    ones[0] = 1.0
-    xt = DeviceVector.from_planes(ones)
-    b = DeviceVector(k, n)
-    nat.check(L.mpcore_mat_vec(A0.handle, xt.handle, b.handle), "mat_vec")
-    W = DeviceMatrix(k, n, n + 1)
-    x = DeviceVector(k, n)
-    a0p, bp, wp, xp = (A0.device_ptr(), b.device_ptr(), W.device_ptr(),
-                       x.device_ptr())
-    sw = np.zeros(n, dtype=np.int32)
-    sstep = ctypes.c_int32()
-
-    def step():
-        nat.check(L.mpcore_dev_copy2d(k, n, n, wp, n + 1, n * (n + 1), a0p, n,
-                                      n * n), "restore A")
-        nat.check(L.mpcore_dev_copy2d(k, n, 1, wp + n * 8, n + 1, n * (n + 1),
-                                      bp, 1, n), "restore b")
-        nat.check(L.mpcore_dev_solve_system(
-            k, n, wp, n + 1, n * (n + 1), 0, xp,
-            sw.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-            ctypes.byref(sstep)), "solve_system")
-
-    for _ in range(args.warmup):
-        step()
-    nat.sync()
-    timer = nat.StreamTimer()
-    with ClockSampler(0) as clk:
-        timer.start()
-        for _ in range(args.steps):
-            step()
-        ms = timer.stop() / args.steps
-        nat.sync()
-    xs = x.download()
-    err = float(np.max(np.abs((xs[0] - 1.0) + xs[1])))
-    flops = (2.0 / 3.0) * n ** 3
-    wc = work_counts(n, k)
-    line = {
-        "metric": "%s LU+solve eff. GFLOP/s ((2/3)n^3/s)" % NAMES[k],
-        "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s",
-        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None,
-        "dtype": "f64x%d (%s, bit-exact EFT arithmetic)" % (k, NAMES[k]),
-        "data": "synthetic (seeded recipe, SURVEY 8d; seed %d)" % seed,
-        "config": {"workload": "config4: distributed %s LU+PP+solve n=%d"
-                   % (NAMES[k], n), "n": n, "k": k, "nb": 32,
-                   "parallelism": "one GPU: the one-rank column-block-cyclic "
-                   "layout is the plain layout; one-call LU + solve "
-                   "(--dist-protocol runs the distributed driver instead)",
-                   "l2": "A restored from a pristine copy each step (>> L2)"},
-        "check": {"max_abs_err_x_vs_ones": err},
-        "roofline": {"bound": "fp64",
-                     "achieved": wc["instr"] / (ms * 1e-3) / 1e12,
-                     "unit": "T FP64 instr/s", "peak": 18.2,
-                     "frac": wc["instr"] / (ms * 1e-3) / 18.2e12,
-                     "traffic": None},
-        "e2e": None, "gpu_launches": None,
-        "clocks": clk.summary(),
-    }
-    print(json.dumps(line))
+def config4_work(n, nb):
+    """madds of config 4's trailing updates (K = nb) and the FP64
+    instructions of the whole LU + solve."""
+    upd = 0
+    for J in range(0, n, nb):
+        w = min(nb, n - J)
+        rest = n - J - w
+        upd += rest * rest * w
+    return upd
 
 
 def run_dist(args):
-    """BASELINE config 4: distributed DD LU (+ solve) of one n x n system,
-    column-block-cyclic over the ranks (nb = 256), NCCL panel + pivot
-    broadcast; factors gathered to rank 0 for the solve.  Strong scaling:
-    the whole system is fixed, value = (2/3) n^3 / (max-over-ranks time)."""
+    """BASELINE config 4: distributed DD LU + solve of ONE n x n system
+    (n = 32768, ~17 GB in DD), column-block-cyclic over the ranks (nb =
+    256), through the native driver (libmpcore dist.cu: one C-ABI call per
+    solve; NCCL panel + pivot broadcasts of the live rows, look-ahead,
+    column-cyclic back substitution; b rides along as a replicated column).
+    One process per GPU; N = 1 runs the same code with a one-rank world.
+    Strong scaling: value = (2/3) n^3 / (max-over-ranks device time)."""
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -509,114 +539,166 @@ def run_dist(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     os.environ.setdefault("MPCORE_DEVICE", str(local))
-    if not dist.is_initialized():
+    if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
-        # NCCL announces itself on stdout at its first communicator: keep
-        # stdout for the one JSON line
-        with stdout_to_stderr():
-            dist.init_process_group("nccl", rank=rank, world_size=world,
-                                    device_id=torch.device("cuda", local))
-            dist.barrier()
+        # host plumbing only (id exchange, timing max): the data path is
+        # libmpcore's own NCCL communicator
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    pg = dist if world > 1 else None
     from paper_2107_12550_b200 import _native as nat
-    from paper_2107_12550_b200.dist import (DeviceBackend, Layout, TorchComm,
-                                            dist_lu_factor)
+    from paper_2107_12550_b200.dist import (DeviceBackend, Layout, NcclComm,
+                                            dist_lu_solve)
     k, n, nb = args.k, args.n, args.dist_nb
     seed = 210712550 + 4
     layout = Layout(n, nb, world)
     be = DeviceBackend(k)
-    lc = layout.local_cols(rank)
-    M = be.alloc(n, lc)
-    be.generate(M, layout, rank, 0, seed)
-    M0 = M.clone()
     L = nat.lib()
+    lc = layout.local_cols(rank)
+    # b = A x_true (x_true = ones, DD mat_vec in the reference's order) on
+    # rank 0 from the full matrix, shared with every rank (setup, untimed)
+    bh = torch.zeros((k, n), dtype=torch.float64)
     if rank == 0:
-        # b = A x_true in DD (x_true = ones; config 0 recipe), full A
-        full = M if world == 1 else be.alloc(n, n)
-        if world > 1:
-            be.generate(full, Layout(n, nb, 1), 0, 0, seed)
+        full = be.alloc(n, n)
+        be.generate(full, Layout(n, nb, 1), 0, 0, seed)
         xt = torch.zeros((k, n), dtype=torch.float64, device="cuda")
         xt[0] = 1.0
-        b = torch.zeros_like(xt)
-        x = torch.zeros_like(xt)
+        bd = torch.zeros_like(xt)
         torch.cuda.synchronize()
         nat.check(L.mpcore_dev_matvec(k, n, n, full.data_ptr(), n, n * n,
-                                      xt.data_ptr(), b.data_ptr()), "matvec")
-    comm = TorchComm()
-    recv = be.alloc(n, layout.local_cols(1)) if (rank == 0 and world > 1) \
-        else None
+                                      xt.data_ptr(), bd.data_ptr()), "matvec")
+        bh = bd.cpu()
+        del full, xt, bd
+        torch.cuda.empty_cache()
+    if pg is not None:
+        pg.broadcast(bh, src=0)
+    M0 = be.alloc(n, lc + 1)
+    base, ld, plane = be.view(M0)
+    torch.cuda.synchronize()      # (torch's zero fill before the generator)
+    if lc > 0:
+        nat.check(L.mpcore_dev_generate_cyclic(
+            k, base, ld, plane, n, lc, nb, world, rank, 0, n, seed),
+            "generate_cyclic")
+    M0[:, :, lc] = bh.to(M0.device)
+    M = M0.clone()
+    torch.cuda.synchronize()
+    x = torch.zeros((k, n), dtype=torch.float64, device=M.device)
+    comm = NcclComm(world, rank)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
 
-    def step():
+    def step(phases=False):
         M.copy_(M0)
-        torch.cuda.synchronize()
-        swaps = dist_lu_factor(be, comm, layout, {rank: M})
-        if world > 1:
-            if rank == 0:
-                full[:, :, torch.as_tensor(layout.global_columns(0),
-                                           device="cuda")] = M
-                for q in range(1, world):
-                    buf = recv[:, :, :layout.local_cols(q)].contiguous()
-                    dist.recv(buf, src=q)
-                    full[:, :, torch.as_tensor(layout.global_columns(q),
-                                               device="cuda")] = buf
-            else:
-                dist.send(M, dst=0)
-        if rank == 0:
-            torch.cuda.synchronize()
-            sw = np.ascontiguousarray(swaps, dtype=np.int32)
-            nat.check(L.mpcore_dev_lu_solve(k, n, full.data_ptr(), n, n * n,
-                                            nat.iptr(sw), b.data_ptr(),
-                                            x.data_ptr()), "solve")
-        torch.cuda.synchronize()
+        return dist_lu_solve(layout, {rank: M}, {rank: x}, k, comm=comm,
+                             stream=sp, phases=phases)
 
     for _ in range(args.warmup):
         step()
-    dist.barrier()
     torch.cuda.synchronize()
-    # CUDA events on the library stream bracket the K steps (each step ends
-    # synchronised, so the stop event closes the whole step sequence)
-    timer = nat.StreamTimer()
+    peak_add, peak_fma = nat.fp64_peak()
+    if pg is not None:
+        pg.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), \
+        torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
-        timer.start()
+        ev0.record(stream)
+        launches = 0
         for _ in range(args.steps):
-            step()
+            launches += step()[2]
+        ev1.record(stream)
         torch.cuda.synchronize()
-        dev_total = timer.stop()
-        dist.barrier()
-    t = torch.tensor([dev_total], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item()) / args.steps
-    if rank == 0:
-        xs = x.cpu().numpy()
-        err = float(np.max(np.abs((xs[0] - 1.0) + xs[1])))
-        flops = (2.0 / 3.0) * n ** 3
-        wc = work_counts(n, k)
-        line = {
-            "metric": "%s LU+solve eff. GFLOP/s ((2/3)n^3/s)" % NAMES[k],
-            "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None,
-            "dtype": "f64x%d (%s, bit-exact EFT arithmetic)" % (k, NAMES[k]),
-            "data": "synthetic (seeded recipe, SURVEY 8d; seed %d)" % seed,
-            "config": {"workload": "config4: distributed %s LU+PP+solve n=%d"
-                       % (NAMES[k], n), "n": n, "k": k, "nb": nb,
-                       "parallelism": "column-block-cyclic x%d, NCCL panel "
-                       "+ pivot broadcast, gather + solve on rank 0" % world,
-                       "l2": "A restored from a pristine copy each step "
-                             "(>> L2)"},
-            "check": {"max_abs_err_x_vs_ones": err},
-            "roofline": {"bound": "fp64",
-                         "achieved": wc["instr"] / (ms * 1e-3) / 1e12 / world,
-                         "unit": "T FP64 instr/s per GPU",
-                         "peak": 18.2, "frac": wc["instr"] / (ms * 1e-3) /
-                         18.2e12 / world, "traffic": None},
-            "e2e": None, "gpu_launches": None,
-            "clocks": clk.summary(),
-        }
-        print(json.dumps(line))
-    dist.barrier()
-    dist.destroy_process_group()
+    ms = max_over_ranks(pg, ev0.elapsed_time(ev1) / args.steps)
+    # per-panel critical-path breakdown: one more step with phase events
+    _, phases, _ = step(phases=True)
+    torch.cuda.synchronize()
+    xs = x.cpu().numpy()
+    # end to end: this rank's columns from page-locked host memory each
+    # step (H2D inside the timed region), solve, x back to the host
+    e2e = None
+    if not args.no_e2e:
+        try:
+            import psutil
+            room = psutil.virtual_memory().available > 3 * M0.numel() * 8
+        except Exception:
+            room = False
+        if room:
+            hM = torch.empty(M0.shape, dtype=torch.float64, pin_memory=True)
+            hM.copy_(M0.cpu())
+            hx = torch.empty((k, n), dtype=torch.float64, pin_memory=True)
+            if pg is not None:
+                pg.barrier()
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            e_steps = max(1, min(args.steps, 2))
+            for _ in range(e_steps):
+                M.copy_(hM, non_blocking=True)
+                dist_lu_solve(layout, {rank: M}, {rank: x}, k, comm=comm,
+                              stream=sp)
+                hx.copy_(x, non_blocking=True)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            e_ms = max_over_ranks(pg, ev0.elapsed_time(ev1) / e_steps)
+            assert hx.numpy().tobytes() == xs.tobytes()
+            e2e = {"value": (2.0 / 3.0) * n ** 3 / (e_ms * 1e-3) / 1e9,
+                   "unit": "GFLOP/s", "ms_per_step": e_ms,
+                   "h2d_bytes_per_step": M0.numel() * 8,
+                   "d2h_bytes_per_step": k * n * 8,
+                   "path": "torch pinned host tensor -> this rank's local "
+                           "columns + b (H2D, every step), mpcore_dist_lu_"
+                           "solve (C ABI), x -> pinned host"}
+    comm.close()
+    if rank != 0:
+        if pg is not None:
+            pg.barrier()
+        return
+    err = float(np.max(np.abs((xs[0] - 1.0) + xs[1])))
+    flops = (2.0 / 3.0) * n ** 3
+    wc = work_counts(n, k)
+    upd_instr = config4_work(n, nb) * MADD_INSTR[k]
+    cpu = None
+    if not args.no_cpu and world == 1:
+        cpu = cpu_baseline(k, args.cpu_n or 4096, seed=seed)
+        cpu["sample"] += ("; rate at n=%d stands for n=%d (time x (n/%d)^3)"
+                          % (args.cpu_n or 4096, n, args.cpu_n or 4096))
+    line = {
+        "metric": "%s LU+solve eff. GFLOP/s ((2/3)n^3/s)" % NAMES[k],
+        "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64x%d (%s, bit-exact EFT arithmetic)" % (k, NAMES[k]),
+        "data": "synthetic (seeded recipe, SURVEY 8d; seed %d)" % seed,
+        "config": config_dict(args, world),
+        "check": {"max_abs_err_x_vs_ones": err},
+        "roofline": {
+            "bound": "fp64",
+            "kernel": "trailing update (gemm_kernel NEG_A, K = %d), rank 0"
+                      % nb,
+            "achieved": upd_instr / world / (phases["update"] * 1e-3) / 1e12
+            if phases["update"] > 0 else None,
+            "peak": peak_add / 1e12, "unit": "T FP64 instr/s per GPU",
+            "frac": upd_instr / world / (phases["update"] * 1e-3) / peak_add
+            if phases["update"] > 0 and peak_add else None,
+            "peak_source": "measured DADD issue rate (mpcore_fp64_peak)",
+            "whole_step_frac": wc["instr"] / (ms * 1e-3) / world / peak_add
+            if peak_add else None,
+            "traffic": None},
+        "phases_ms_rank0": phases,
+        "phases_note": "one extra step with CUDA events around every phase "
+                       "of every panel on its own stream (factor + pack: "
+                       "side stream; bcast: comm stream incl. waiting for "
+                       "the root; exch_trsm, update, back: main stream); "
+                       "overlapping streams, so the parts exceed the total",
+        "e2e": e2e,
+        "gpu_launches": int(launches / max(1, args.steps)),
+        "clocks": clk.summary(),
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line))
+    if pg is not None:
+        pg.barrier()
 
 
 def run_config1(args):
@@ -675,19 +757,21 @@ def run_config1(args):
         nat.set_planes_async(EA[slot].handle, hA.array)
         nat.set_planes_async(EB[slot].handle, hB.array)
 
-    def e2e_step(i):
-        upload((i + 1) % 2)
+    def e2e_step(i, last=False):
+        if not last:
+            upload((i + 1) % 2)
         nat.check(L.mpcore_mat_mul(EA[i % 2].handle, EB[i % 2].handle,
                                    EC[i % 2].handle), "mm")
         nat.get_planes_async(EC[i % 2].handle, hCs[i % 2].array)
 
     upload(0)
-    e2e_step(0)
+    e2e_step(0, last=True)                        # warm-up
     nat.sync()
-    e_steps = max(1, min(args.steps, 3))
+    e_steps = args.steps
     timer.start()
+    upload(1)             # every timed step's A and B cross inside the region
     for i in range(1, e_steps + 1):
-        e2e_step(i)
+        e2e_step(i, last=i == e_steps)
     nat.sync()                                    # the last C is on the host
     e2e_ms = max_over_ranks(pg, timer.stop() / e_steps)
     hC = hCs[e_steps % 2]
@@ -706,9 +790,7 @@ def run_config1(args):
         "dtype": "f64x%d (%s, bit-exact EFT arithmetic)" % (k, NAMES[k]),
         "data": "synthetic (seeded splitmix64 recipe, SURVEY 8d; seed %d)"
                 % seed,
-        "config": {"workload": "config1: %s GEMM n=%d" % (NAMES[k], n),
-                   "n": n, "k": k, "parallelism": "replicas x%d" % world,
-                   "l2": "A, B, C = 3 x %d MB (> L2)" % (k * n * n * 8 >> 20)},
+        "config": config_dict(args, world),
         "e2e": {"value": world * flops / (e2e_ms * 1e-3) / 1e9,
                 "unit": "GFLOP/s", "ms_per_step": e2e_ms,
                 "h2d_bytes_per_step": 2 * k * n * n * 8,
@@ -773,9 +855,7 @@ def run_config3(args):
         "data": "synthetic: A = U diag(sigma) W, sigma geometric 1..1e-30, "
                 "U, W seeded butterfly-orthogonal at 576-bit fixed point "
                 "(stands in for QR of a Gaussian, SURVEY 7); b = A*ones",
-        "config": {"workload": "config3: TD-mpmath IR n=%d kappa=1e30" % n,
-                   "n": n, "long_bits": 512, "rtol": "1e-100", "atol": "0",
-                   "maxtimes": 20, "parallelism": "replicas x%d" % world},
+        "config": config_dict(args, world),
         "result": {"iterations": r["iterations"],
                    "stop_reason": r["stop_reason"],
                    "residuals": r["residuals"],
@@ -821,17 +901,22 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4])
+    ap.add_argument("--config", type=int, default=None, choices=[1, 2, 3, 4],
+                    help="BASELINE config (default: 2 on one GPU; 4 -- the "
+                         "distributed n=32768 DD LU, strong scaling -- when "
+                         "launched on several GPUs)")
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--dim", dest="n", type=int, default=None)
     ap.add_argument("--nb", type=int, default=0)
     ap.add_argument("--dist-nb", type=int, default=256)
     ap.add_argument("--cpu-n", type=int, default=0,
-                    help="CPU baseline sample size (0: the workload n)")
+                    help="CPU baseline sample size (0: per config)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--dist-protocol", action="store_true",
-                    help="config 4 at one GPU through the distributed driver")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
+    if args.config is None:
+        multi = int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.gpus > 1
+        args.config = 4 if multi else 2
     if args.config == 4:
         args.k = args.k or 2
         args.n = args.n or 32768
@@ -847,11 +932,7 @@ def main():
     if args.impl == "reference":
         run_reference(args)
     elif args.config == 4:
-        if int(os.environ.get("WORLD_SIZE", "1")) == 1 and \
-                not args.dist_protocol:
-            run_single_config4(args)
-        else:
-            run_dist(args)
+        run_dist(args)
     elif args.config == 3:
         run_config3(args)
     elif args.config == 1:

@@ -255,8 +255,8 @@ int32_t mpcore_dist_comm_destroy(uint64_t comm);
  * rank i: ranks[i], the local matrix at bases[i] (lds[i], planes[i]) with
  * cols[i] = its local column count + 1, the last column holding b on
  * entry (y = L^-1 P b on exit), and xs[i] (device, k*n planar) for x.
- * The work starts after `stream`'s queued work (0: the library stream) and
- * that stream waits for its end.  swaps_out (host, n) = PivotRecord.swaps;
+ * The work starts after `stream`'s queued work (0: the library stream; 1:
+ * cudaStreamLegacy) and that stream waits for its end.  swaps_out (host, n) = PivotRecord.swaps;
  * phase_ms (6, optional, one served rank only): total, tall-block factor +
  * pack, broadcasts, exchanges + U12, trailing update, back substitution;
  * launches (optional): kernels + collectives enqueued.  3 = singular. */

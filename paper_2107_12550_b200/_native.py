@@ -11,7 +11,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpcore.so")
+LIB_PATH = os.environ.get("MPCORE_LIB") or os.path.join(_HERE, "libmpcore.so")  # (A/B builds)
 
 OK, BAD_HANDLE, BAD_DIMENSION, SINGULAR, BAD_PARSE, OVERFLOW, INTERNAL = \
     range(7)
@@ -165,7 +165,11 @@ def lib():
                         % LIB_PATH)
                 L = ctypes.CDLL(LIB_PATH)
                 for name, (res, args) in _PROTOS.items():
-                    f = getattr(L, name)
+                    f = getattr(L, name, None)
+                    if f is None and os.environ.get("MPCORE_LIB"):
+                        continue   # an older A/B build
+                    if f is None:
+                        raise ImportError("libmpcore lacks " + name)
                     f.restype = res
                     f.argtypes = args
                 _lib = L

@@ -542,6 +542,9 @@ int dist_lu_solve(void *comm, int k, int n, int nb, int G,
   }
   DistWork &DW = dist_work();
   while ((int)DW.ranks.size() < R) DW.ranks.emplace_back(new RankWork);
+  // diagnostics: MPCORE_DIST_SERIAL=1 runs every stream's work in order on
+  // the main stream (no look-ahead overlap)
+  static const bool serial = std::getenv("MPCORE_DIST_SERIAL") != nullptr;
   if (!DW.S2) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -603,23 +606,24 @@ int dist_lu_solve(void *comm, int k, int n, int nb, int G,
     RankWork &rw = *DW.ranks[i];
     const int J = P * nb, w = width(P), off = local_off(P), s = P % 2;
     const DistRankView &V = views[i];
+    cudaStream_t S2 = serial ? rw.S : DW.S2;
     if ((e = cudaEventRecord(rw.ev_blk, rw.S)) ||
-        (e = cudaStreamWaitEvent(DW.S2, rw.ev_blk, 0)) ||
-        (e = cudaStreamWaitEvent(DW.S2, rw.ev_consumed[s], 0)))
+        (e = cudaStreamWaitEvent(S2, rw.ev_blk, 0)) ||
+        (e = cudaStreamWaitEvent(S2, rw.ev_consumed[s], 0)))
       return fail(e, "factor order");
-    ph.begin(DIST_FACTOR, DW.S2);
+    ph.begin(DIST_FACTOR, S2);
     MatView blk = at(V.A, J, off);
-    if ((e = lu_factor_async(k, n - J, w, blk, rw.tswaps, 32, ws, DW.S2)))
+    if ((e = lu_factor_async(k, n - J, w, blk, rw.tswaps, 32, ws, S2)))
       return fail(e, "tall-block LU");
     int32_t *hdr = reinterpret_cast<int32_t *>(rw.slot[s]);
-    panel_header_kernel<<<1, 256, 0, DW.S2>>>(hdr, rw.tswaps, ws.status, J,
+    panel_header_kernel<<<1, 256, 0, S2>>>(hdr, rw.tswaps, ws.status, J,
                                               w, n);
     if ((e = cudaGetLastError())) return fail(e, "panel header");
     if ((e = copy2d(k, n - J, w, slot_planes(rw, s), w, (int64_t)(n - J) * w,
-                    blk.p, V.A.ld, V.A.plane, DW.S2)))
+                    blk.p, V.A.ld, V.A.plane, S2)))
       return fail(e, "pack");
-    ph.end(DIST_FACTOR, DW.S2);
-    if ((e = cudaEventRecord(DW.ev_packed, DW.S2)) ||
+    ph.end(DIST_FACTOR, S2);
+    if ((e = cudaEventRecord(DW.ev_packed, S2)) ||
         (e = cudaStreamWaitEvent(rw.C, DW.ev_packed, 0)))
       return fail(e, "pack order");
     nlaunch += 2;

@@ -387,7 +387,7 @@ class NcclComm:
             self.handle = 0
 
 
-def dist_lu_solve(layout, local, xs, k, comm=None, stream=0, phases=False):
+def dist_lu_solve(layout, local, xs, k, comm=None, stream=None, phases=False):
     """Factor the distributed matrix and solve (one library call).
 
     local: {rank: device tensor (k, n, local_cols + 1)}, the last column
@@ -395,10 +395,16 @@ def dist_lu_solve(layout, local, xs, k, comm=None, stream=0, phases=False):
     (k, n)} receiving x.  comm: an NcclComm (this process serves its one
     rank) or None (every rank of the layout served here on one device).
     stream: the CUDA stream (int handle) the work is ordered after and that
-    waits for it (0: the library stream).  Returns (swaps, phase_ms or
+    waits for it; default: torch's current stream (the legacy default
+    stream is passed as cudaStreamLegacy).  Returns (swaps, phase_ms or
     None, launches); raises SingularMatrixError(step) like lu_factor_pp."""
     ranks = sorted(local)
     R = len(ranks)
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream().cuda_stream
+    if stream == 0:
+        stream = 1          # cudaStreamLegacy: torch's legacy default stream
     arr = lambda t, vals: (t * R)(*vals)  # noqa: E731
     for r in ranks:
         M = local[r]
