@@ -295,6 +295,41 @@ class Handle:
         self.h = 0
 
 
+_DEVICE_OK = None
+
+
+def device_available():
+    """True when libmpcore is built and finds its sm_100 device (cached)."""
+    global _DEVICE_OK
+    if _DEVICE_OK is None:
+        try:
+            v = _i32()
+            _DEVICE_OK = lib().mpcore_sm_count(ctypes.byref(v)) == OK
+        except Exception:
+            _DEVICE_OK = False
+    return _DEVICE_OK
+
+
+class _PinnedHolder:
+    """numpy base object keeping a PinnedBuffer alive (array interface)."""
+
+    def __init__(self, pb, shape):
+        self._pb = pb
+        self.__array_interface__ = {
+            "shape": tuple(shape), "typestr": "<f8",
+            "data": (pb.ptr.value, False), "version": 3}
+
+
+def pinned_zeros(shape):
+    """float64 zeros in page-locked host memory (mpcore_host_alloc): the
+    containers' planes, so every host<->device copy of the drop-in API runs
+    at DMA speed.  The memory lives as long as the returned array."""
+    pb = PinnedBuffer(shape)
+    a = np.asarray(_PinnedHolder(pb, pb.shape))
+    a[...] = 0.0
+    return a
+
+
 class PinnedBuffer:
     """Page-locked host array (mpcore_host_alloc) viewed as numpy."""
 

@@ -127,10 +127,25 @@ class McDomain:
         return value.to_components(self.k)
 
 
+# containers at least this large keep their planes page-locked (when the
+# device is present), so lu_factor_pp / lu_solve / mat_mul_blocked move
+# them at DMA speed instead of through pageable staging
+PINNED_MIN_BYTES = 1 << 20
+
+
 def _planes_zeros(k, shape):
     if isinstance(shape, int):
         shape = (shape,)
-    return np.zeros((k,) + tuple(shape), dtype=np.float64)
+    shape = (k,) + tuple(shape)
+    if 8 * int(np.prod(shape)) >= PINNED_MIN_BYTES and nat.device_available():
+        return nat.pinned_zeros(shape)
+    return np.zeros(shape, dtype=np.float64)
+
+
+def _planes_copy(a):
+    out = _planes_zeros(a.shape[0], a.shape[1:])
+    out[...] = a
+    return out
 
 
 class Vector:
@@ -171,7 +186,7 @@ class Vector:
 
     def copy(self):
         if self.domain.kind == "mc":
-            return Vector(self.domain, self.n, self.data.copy())
+            return Vector(self.domain, self.n, _planes_copy(self.data))
         return Vector(self.domain, self.n, list(self.data))
 
     def to_list(self):
@@ -227,7 +242,7 @@ class DenseMatrix:
     def copy(self):
         if self.domain.kind == "mc":
             return DenseMatrix(self.domain, self.rows, self.cols,
-                               self.data.copy())
+                               _planes_copy(self.data))
         return DenseMatrix(self.domain, self.rows, self.cols,
                            [list(r) for r in self.data])
 

@@ -26,7 +26,9 @@ keys = [
     ("DRAM throughput (% elapsed)", "dram__throughput.avg.pct_of_peak_sustained_elapsed"),
     ("L2 hit rate", "lts__t_sector_hit_rate.pct"),
     ("achieved occupancy", "sm__warps_active.avg.pct_of_peak_sustained_active"),
-    ("FP64 instructions executed", "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum"),
+    ("DADD thread-instructions", "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum"),
+    ("DMUL thread-instructions", "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum"),
+    ("DFMA thread-instructions", "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum"),
 ]
 for label, key in keys:
     print("%-48s %s" % (label, g(key)))
