@@ -271,6 +271,13 @@ int32_t mpcore_dist_lu_solve(uint64_t comm, int32_t k, int32_t n, int32_t nb,
 
 /* ---- extensions: device, diagnostics, profiling ------------------------ */
 
+/* debug (the substitute for compute-sanitizer memcheck, which this pool
+ * does not allow): with MPCORE_DEBUG_GUARD=1 in the environment when an
+ * object is created, its planes sit between two 64 KiB guard zones filled
+ * with 0xA5; this checks every live guarded object: *checked of them,
+ * *bad with a written zone */
+int32_t mpcore_debug_check_guards(int64_t *checked, int64_t *bad);
+
 /* select the CUDA device for this process (before any other call) */
 int32_t mpcore_set_device(int32_t device);
 int32_t mpcore_device_name(char *out, int32_t cap);

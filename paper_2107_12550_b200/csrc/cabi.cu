@@ -50,12 +50,18 @@ struct Object {
   // has not yet been made to wait for it; set and cleared only under the
   // device lock
   std::atomic<bool> upload_pending{false};
+  // MPCORE_DEBUG_GUARD: planes allocated inside guard zones (raw = base
+  // of the allocation, d = raw + guard) filled with GUARD_BYTE; checked by
+  // mpcore_debug_check_guards
+  char *raw = nullptr;
+  size_t guard = 0;
   ~Object() {
     if (upload) {  // an asynchronous upload may still target d
       cudaEventSynchronize(upload);
       cudaEventDestroy(upload);
     }
-    if (d) cudaFree(d);
+    if (raw) cudaFree(raw);
+    else if (d) cudaFree(d);
     if (dswaps) cudaFree(dswaps);
     if (dperm) cudaFree(dperm);
   }
@@ -259,6 +265,12 @@ mpk::MatView view(const ObjPtr &o) {
   return v;
 }
 
+constexpr int kGuardByte = 0xA5;
+size_t debug_guard_bytes() {
+  const char *g = std::getenv("MPCORE_DEBUG_GUARD");
+  return g && *g && *g != '0' ? (size_t)64 * 1024 : 0;
+}
+
 int new_container(int kind, int k, int rows, int cols, uint64_t *out) {
   if (out == nullptr) return MPCORE_BAD_DIMENSION;
   *out = 0;
@@ -272,8 +284,19 @@ int new_container(int kind, int k, int rows, int cols, uint64_t *out) {
   o->rows = rows;
   o->cols = cols;
   size_t bytes = (size_t)o->count() * sizeof(double);
-  cudaError_t e = cudaMalloc(&o->d, bytes);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  cudaError_t e;
+  if (const size_t g = debug_guard_bytes()) {
+    // debug: guard zones on both sides of the planes (write-overrun check)
+    e = cudaMalloc(&o->raw, bytes + 2 * g);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    o->guard = g;
+    o->d = reinterpret_cast<double *>(o->raw + g);
+    cudaMemsetAsync(o->raw, kGuardByte, g, device().stream);
+    cudaMemsetAsync(o->raw + g + bytes, kGuardByte, g, device().stream);
+  } else {
+    e = cudaMalloc(&o->d, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  }
   e = cudaMemsetAsync(o->d, 0, bytes, device().stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemset");
   int st = finish("matrix_new");
@@ -1977,6 +2000,43 @@ int32_t mpcore_dist_lu_solve(uint64_t comm, int32_t k, int32_t n, int32_t nb,
   if (st == 2) return fail(MPCORE_BAD_DIMENSION, err);
   if (st == 3) return fail(MPCORE_SINGULAR, err);
   if (st) return fail(MPCORE_INTERNAL, err);
+  return MPCORE_OK;
+}
+
+
+// Debug: verify every guarded object's guard zones (MPCORE_DEBUG_GUARD=1 at
+// allocation).  *checked = objects with guards, *bad = objects whose zones
+// were written.
+int32_t mpcore_debug_check_guards(int64_t *checked, int64_t *bad) {
+  if (!checked || !bad) return MPCORE_BAD_DIMENSION;
+  *checked = *bad = 0;
+  std::vector<ObjPtr> objs;
+  {
+    Table &T = table();
+    std::lock_guard<std::mutex> g(T.mu);
+    for (auto &kv : T.map)
+      if (kv.second->raw) objs.push_back(kv.second);
+  }
+  DevLock L;
+  if (L.st) return L.st;
+  for (auto &o : objs) {
+    const size_t g = o->guard, bytes = (size_t)o->count() * sizeof(double);
+    std::vector<unsigned char> h(2 * g);
+    cudaError_t e = cudaMemcpyAsync(h.data(), o->raw, g,
+                                    cudaMemcpyDeviceToHost, device().stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h.data() + g, o->raw + g + bytes, g,
+                          cudaMemcpyDeviceToHost, device().stream);
+    int st = finish("guards");
+    if (st) return st;
+    if (e != cudaSuccess) return cuda_fail(e, "guards");
+    ++*checked;
+    for (unsigned char c : h)
+      if (c != kGuardByte) {
+        ++*bad;
+        break;
+      }
+  }
   return MPCORE_OK;
 }
 

@@ -765,7 +765,16 @@ int dist_lu_solve(void *comm, int k, int n, int nb, int G,
       return fail(e, "y");
   }
   const size_t vbytes = (size_t)k * n * sizeof(double);
-  for (int b = nbk - 1; b >= 0; --b) {
+  if (G == 1) {
+    // one rank holds all of U: the one-GPU pipelined sweep over the whole
+    // triangle (the same per-element chain, rows in one cooperative launch
+    // instead of one launch per block)
+    RankWork &rw = *DW.ranks[0];
+    if ((e = lu_solve_back(k, n, views[0].A, rw.v, sw, rw.S)))
+      return fail(e, "back substitution");
+    ++nlaunch;
+  }
+  for (int b = G == 1 ? -1 : nbk - 1; b >= 0; --b) {
     const int o = owner(b), J = b * nb, w = width(b), off = local_off(b);
     if (b < nbk - 1 && owner(b + 1) != o) {
       const int po = owner(b + 1), ip = idx_of[po], io = idx_of[o];
