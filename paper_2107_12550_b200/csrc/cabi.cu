@@ -681,6 +681,9 @@ struct IrWorkspace {
   size_t stagecap = 0, hcap = 0, stage_plcap = 0;
   void *rA = nullptr, *rb = nullptr, *rx = nullptr, *rres = nullptr;
   size_t rAcap = 0, rbcap = 0, rxcap = 0, rrcap = 0;
+  // page-locked results of an asynchronous factor_solve: status, swaps, x
+  void *hres_fs = nullptr;
+  size_t hres_fscap = 0;
   cudaStream_t up = nullptr;
   cudaEvent_t up_done = nullptr;
 };
@@ -710,6 +713,16 @@ cudaError_t grow_host(void **p, size_t &cap, size_t need) {
 IrWorkspace &ir_ws() {
   static IrWorkspace w;
   return w;
+}
+
+// production variant of the long residual (residual.cu): 2 = products off
+// the chain (default), 0 = warp per row; MPCORE_RESIDUAL_VARIANT overrides
+int residual_variant() {
+  static const int v = [] {
+    const char *e = std::getenv("MPCORE_RESIDUAL_VARIANT");
+    return e ? std::atoi(e) : 2;
+  }();
+  return v;
 }
 
 // The IR's short side on the GPU: factors stay resident in HBM.
@@ -825,6 +838,105 @@ class GpuShortSolver : public mpr::ShortSolver {
     }
     return MPCORE_OK;
   }
+  // the same, asynchronously: the uploads, the LU of [A | b], the back
+  // substitution and the copies of status, swaps and x into page-locked
+  // memory are enqueued and begin returns; end waits for them
+  int factor_solve_begin(int k, int n, const double *a,
+                         const std::vector<double> &b,
+                         std::string &err) override {
+    if (!claim()) return -1;
+    k_ = k;
+    n_ = n;
+    DevLock L;
+    if (L.st) { err = g_err; return L.st; }
+    Device &D = device();
+    IrWorkspace &w = ir_ws();
+    cudaError_t e = cudaSuccess;
+    const size_t plane = (size_t)n * (n + 1);
+    const size_t mb = (size_t)k * plane * sizeof(double), vb = (size_t)k * n * 8;
+    const size_t hb = 16 + (size_t)n * 4 + vb;
+    if ((e = ensure_buffers(mb, vb, (size_t)n * 4)) == cudaSuccess)
+      e = grow_host(&w.hres_fs, w.hres_fscap, hb);
+    if (e == cudaSuccess && D.swaps_cap < n) {
+      if (D.dswaps) cudaFree(D.dswaps);
+      D.dswaps = nullptr;
+      D.swaps_cap = 0;
+      if ((e = cudaMalloc(&D.dswaps, (size_t)n * sizeof(int32_t))) ==
+          cudaSuccess)
+        D.swaps_cap = n;
+    }
+    for (int c = 0; c < k && e == cudaSuccess; ++c) {
+      e = cudaMemcpy2DAsync(a_ + c * plane, (n + 1) * 8, a + (size_t)c * n * n,
+                            (size_t)n * 8, (size_t)n * 8, n,
+                            cudaMemcpyHostToDevice, D.stream);
+      if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(a_ + c * plane + n, (n + 1) * 8,
+                              b.data() + (size_t)c * n, 8, 8, n,
+                              cudaMemcpyHostToDevice, D.stream);
+    }
+    char *h = static_cast<char *>(w.hres_fs);
+    mpk::MatView v{a_, n + 1, (int64_t)plane};
+    if (e == cudaSuccess)
+      e = mpk::lu_factor_async(k, n, n + 1, v, D.dswaps, default_nb(k, n),
+                               D.ws, D.stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h, D.ws.status, 4, cudaMemcpyDeviceToHost,
+                          D.stream);
+    for (int c = 0; c < k && e == cudaSuccess; ++c)
+      e = cudaMemcpy2DAsync(x_ + (size_t)c * n, sizeof(double),
+                            a_ + (size_t)c * plane + n, (size_t)(n + 1) * 8, 8,
+                            n, cudaMemcpyDeviceToDevice, D.stream);
+    // (the back substitution reads garbage after a singular step; end
+    // reports the step and never uses it)
+    if (e == cudaSuccess) e = mpk::lu_solve_back(k, n, v, x_, D.sw, D.stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h + 16, D.dswaps, (size_t)n * 4,
+                          cudaMemcpyDeviceToHost, D.stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h + 16 + (size_t)n * 4, x_, vb,
+                          cudaMemcpyDeviceToHost, D.stream);
+    if (e != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
+    ld_ = n + 1;
+    inflight_ = true;
+    return MPCORE_OK;
+  }
+  int factor_solve_end(std::vector<double> &x, std::string &err) override {
+    if (!inflight_) { err = "no factorisation in flight"; return MPCORE_INTERNAL; }
+    inflight_ = false;
+    DevLock L;
+    if (L.st) { err = g_err; return L.st; }
+    Device &D = device();
+    cudaError_t e = cudaStreamSynchronize(D.stream);
+    if (e != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
+    const int n = n_, k = k_;
+    const char *h = static_cast<const char *>(ir_ws().hres_fs);
+    int32_t step;
+    std::memcpy(&step, h, 4);
+    if (step >= 0) {
+      err = "no nonzero pivot at elimination step " + std::to_string(step);
+      return MPCORE_SINGULAR;
+    }
+    const int32_t *swaps = reinterpret_cast<const int32_t *>(h + 16);
+    std::vector<int32_t> order(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    for (int j = 0; j < n; ++j)
+      if (swaps[j] != j) std::swap(order[j], order[swaps[j]]);
+    x.resize((size_t)k * n);
+    std::memcpy(x.data(), h + 16 + (size_t)n * 4, x.size() * sizeof(double));
+    if ((e = cudaMemcpyAsync(perm_, order.data(), (size_t)n * 4,
+                             cudaMemcpyHostToDevice, D.stream)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(D.stream)) != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
+    return MPCORE_OK;
+  }
   // ---- the long residual on the device (residual.cu) ----
   bool residual_supported(int p) override { return p <= 512 && claim(); }
   void *staging(int slot, size_t bytes) override {
@@ -864,6 +976,12 @@ class GpuShortSolver : public mpr::ShortSolver {
     rn_ = n;
     rp_ = p;
     upload_pending_ = true;  // issued once the short matrix is on the GPU
+    if (inflight_) {         // (it already is: the factorisation is running)
+      if ((e = start_upload()) != cudaSuccess) {
+        err = cudaGetErrorString(e);
+        return MPCORE_INTERNAL;
+      }
+    }
     return MPCORE_OK;
   }
   // the long A (page-locked staging) and b to the device, asynchronously:
@@ -901,7 +1019,8 @@ class GpuShortSolver : public mpr::ShortSolver {
       e = cudaMemcpyAsync(w.rx, hx, vb, cudaMemcpyHostToDevice, D.stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(D.stream, w.up_done, 0);
     if (e == cudaSuccess)
-      e = mpk::long_residual(rp_, rn_, w.rA, w.rx, w.rb, w.rres, D.stream);
+      e = mpk::long_residual(rp_, rn_, w.rA, w.rx, w.rb, w.rres, D.stream,
+                             residual_variant());
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(hres, w.rres, vb, cudaMemcpyDeviceToHost, D.stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(D.stream);
@@ -973,6 +1092,7 @@ class GpuShortSolver : public mpr::ShortSolver {
   int k_ = 0, n_ = 0, rn_ = 0, rp_ = 0;
   int ld_ = 0;  // row stride of the factors (n, or n + 1 after factor_solve)
   bool upload_pending_ = false;
+  bool inflight_ = false;  // factor_solve_begin without its end yet
   bool tried_ = false;
   bool shared_ = false;  // buffers borrowed from ir_ws()
   double *a_ = nullptr, *b_ = nullptr, *x_ = nullptr;
@@ -1648,7 +1768,7 @@ int32_t mpcore_debug_panel_trace(uint64_t *out_ns, int64_t cap) {
 int32_t mpcore_debug_long_residual_selftest(int32_t n, int32_t prec,
                                             uint64_t seed, int32_t variant,
                                             int64_t *mismatches) {
-  if (!mismatches || variant < 0 || variant > 1) return MPCORE_BAD_DIMENSION;
+  if (!mismatches || variant < 0 || variant > 3) return MPCORE_BAD_DIMENSION;
   DevLock L;
   if (L.st) return L.st;
   *mismatches = mpr::long_residual_selftest(n, prec, seed, device().stream,

@@ -352,6 +352,14 @@ struct PhaseLog {
   }
 };
 
+// software prefetch of a value's heap-allocated mantissa limbs
+constexpr size_t kPrefetch = 24;
+static inline void prefetch_bf(const BF &v) {
+  const uint32_t *p = v.man.w.data();
+  __builtin_prefetch(p);
+  __builtin_prefetch(p + 16);
+}
+
 int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
                 int short_k, int long_bits, const char *rtol_s,
                 const char *atol_s, int max_iter, int threads, ShortSolver &S,
@@ -432,10 +440,17 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
   };
   std::vector<int> head_emax(T, INT_MIN);
   std::vector<double> head_sum(T, 0.0);
+  // the factorisation can start as soon as the short planes exist: with an
+  // asynchronous short side the fixed-width copy of A (for the device
+  // residual) is written in a second pass while the GPU factors
+  const bool split_factor = std::getenv("MPCORE_REFINE_SPLIT_FACTOR") != nullptr;
+  const bool overlap = fast && dev_res && !split_factor &&
+                       std::getenv("MPCORE_REFINE_NO_OVERLAP") == nullptr;
   if (fast) {
-    // one pass: fixed-width copy, its k binary64 heads (bf_to_multicomp)
-    // and, per thread, the largest head exponent with the sum of the heads'
-    // squares scaled by it (for the ||A||_F bounds below)
+    // one pass: fixed-width value, its k binary64 heads (bf_to_multicomp),
+    // the fixed-width copy (unless a second pass writes it) and, per
+    // thread, the largest head exponent with the sum of the heads' squares
+    // scaled by it (for the ||A||_F bounds below)
     std::vector<char> bad(T, 0);
     std::vector<std::thread> ws;
     for (int t = 0; t < T; ++t)
@@ -445,8 +460,11 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
         int hmax = INT_MIN;
         double hsum = 0.0, hscale = 0.0;
         for (size_t e = a; e < b; ++e) {
+          // the mantissas live on the heap, one allocation each: fetch a
+          // few elements ahead (the pass is bound by those misses)
+          if (e + kPrefetch < b) prefetch_bf(Avals[e + kPrefetch]);
           const ff::F v = ff::from_bf(Avals[e], pi);
-          Af[e] = v;
+          if (!overlap) Af[e] = v;
           if (!ff::to_multicomp(v, k, pi, c) &&
               bn::to_multicomp(ff::to_bf(v), k, c)) {
             bad[t] = 1;
@@ -518,10 +536,29 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
       }
     }
   }
-  plog.mark("A -> fixed, planes");
+  plog.mark(overlap ? "A -> planes" : "A -> fixed, planes");
   if ((st = to_planes(Bvals, k, b_pl.data(), (size_t)n, err))) return st;
   std::vector<ff::F> Bf;
   bool use_dev = false;
+  bool begun = false;
+  if (overlap) {
+    st = S.factor_solve_begin(k, n, a_pl.p, b_pl, err);
+    if (st > 0) return st;
+    begun = st == 0;
+  }
+  auto t1 = Clock::now();
+  if (overlap) {
+    // the fixed-width A, while the GPU factors (or before the synchronous
+    // factorisation when the short side cannot overlap)
+    par_rows(nn, threads, [&](size_t a, size_t b) {
+      for (size_t e = a; e < b; ++e) {
+        if (e + kPrefetch < b) prefetch_bf(Avals[e + kPrefetch]);
+        Af[e] = ff::from_bf(Avals[e], pi);
+      }
+    });
+    plog.mark("A -> fixed (overlapping the factorisation)");
+    if (!begun) t1 = Clock::now();
+  }
   if (fast) {
     Bf.resize(n);
     for (int i = 0; i < n; ++i) Bf[i] = ff::from_bf(Bvals[i], pi);
@@ -530,11 +567,12 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
       use_dev = true;
     }
   }
-  const auto t1 = Clock::now();
   // the factorisation and the first solve (b along the LU on the GPU);
   // MPCORE_REFINE_SPLIT_FACTOR=1 takes factor() + solve() instead (tests:
   // both give the same bits)
-  if (std::getenv("MPCORE_REFINE_SPLIT_FACTOR") != nullptr) {
+  if (begun) {
+    if ((st = S.factor_solve_end(x_pl, err))) return st;
+  } else if (split_factor) {
     if ((st = S.factor(k, n, a_pl.p, err))) return st;
     if ((st = S.solve(b_pl, x_pl, err))) return st;
   } else if ((st = S.factor_solve(k, n, a_pl.p, b_pl, x_pl, err))) {

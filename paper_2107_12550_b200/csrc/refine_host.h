@@ -42,6 +42,15 @@ class ShortSolver {
     const int st = factor(k, n, a_planes, err);
     return st ? st : solve(b_planes, x_planes, err);
   }
+  // Optional, asynchronous form of factor_solve: begin enqueues the
+  // factorisation and the first solve and returns (a_planes and b_planes
+  // must stay valid until end); end waits and delivers x.  begin returning
+  // -1 means "not supported" (the caller uses factor_solve).
+  virtual int factor_solve_begin(int k, int n, const double *a_planes,
+                                 const std::vector<double> &b_planes,
+                                 std::string &err) { return -1; }
+  virtual int factor_solve_end(std::vector<double> &x_planes,
+                               std::string &err) { return 6; }
   // Optional: the long residual b - A x on the device.
   // Values travel as fixed-width long floats (fastfloat.h ff::F, p <= 512).
   virtual bool residual_supported(int p) { return false; }

@@ -68,12 +68,195 @@ long_residual_warp_kernel(const lf::DF *__restrict__ A,
   }
 }
 
+// The same chain with its products moved off it: acc_i = add(acc_i,
+// mul(A_ij, x_j)) needs each product only when it is added, and the
+// products do not depend on acc.  One CTA per row: warp 0 runs the chain of
+// correctly rounded adds in ascending j; warps 1..LR_PROD form the products
+// (the same warp-cooperative mul) ahead of it into a shared-memory ring,
+// published by a per-slot sequence flag.  Every operation and its order are
+// unchanged, so the result is the same bits; the chain is the adds only.
+constexpr int LR_PROD = 3, LR_RING = 8;
+
+__global__ void __launch_bounds__(32 * (1 + LR_PROD))
+long_residual_split_kernel(const lf::DF *__restrict__ A,
+                           const lf::DF *__restrict__ x,
+                           const lf::DF *__restrict__ b,
+                           lf::DF *__restrict__ res, int n, int p) {
+  __shared__ uint64_t ring_m[LR_RING][32];
+  __shared__ int64_t ring_e[LR_RING];
+  __shared__ int ring_s[LR_RING];
+  __shared__ volatile int ready[LR_RING];  // j + 1 once product j is in
+  __shared__ volatile int consumed;        // products taken by the chain
+  const int row = blockIdx.x, warp = threadIdx.x >> 5, t = threadIdx.x & 31;
+  if (threadIdx.x < LR_RING) ready[threadIdx.x] = 0;
+  if (threadIdx.x == 0) consumed = 0;
+  __syncthreads();
+  auto load = [&](const lf::DF &v) {
+    lw::WV w;
+    w.m = t < lf::NL ? v.m[t] : 0ull;
+    w.exp = v.exp;
+    w.sign = v.sign;
+    return w;
+  };
+  const lf::DF *arow = A + (int64_t)row * n;
+  if (warp == 0) {
+    lw::WV acc = lw::zero();
+    for (int j = 0; j < n; ++j) {
+      const int s = j % LR_RING;
+      while (lw::uni(ready[s] != j + 1)) {
+      }
+      __threadfence_block();
+      lw::WV pr;
+      pr.m = ring_m[s][t];
+      pr.exp = ring_e[s];
+      pr.sign = ring_s[s];
+      __threadfence_block();
+      __syncwarp();
+      if (t == 0) consumed = j + 1;  // the slot may be refilled
+      acc = lw::add(acc, pr, p);
+    }
+    const lw::WV r = lw::add(load(b[row]), lw::neg(acc), p);
+    if (t < lf::NL) res[row].m[t] = r.m;
+    if (t == 0) {
+      res[row].sign = r.sign;
+      res[row].exp = r.sign == 0 ? 0 : r.exp;
+    }
+  } else {
+    const int pw = warp - 1;
+    int j = pw;
+    lw::WV an, xn;
+    if (j < n) {
+      an = load(arow[j]);
+      xn = load(x[j]);
+    }
+    for (; j < n; j += LR_PROD) {
+      const lw::WV aj = an, xj = xn;
+      if (j + LR_PROD < n) {
+        an = load(arow[j + LR_PROD]);
+        xn = load(x[j + LR_PROD]);
+      }
+      const lw::WV pr = lw::mul(aj, xj, p);
+      const int s = j % LR_RING;
+      // slot s last held product j - LR_RING
+      while (lw::uni(consumed <= j - LR_RING)) __nanosleep(64);
+      __threadfence_block();
+      ring_m[s][t] = pr.m;
+      if (t == 0) {
+        ring_e[s] = pr.exp;
+        ring_s[s] = pr.sign;
+      }
+      __threadfence_block();
+      __syncwarp();
+      if (t == 0) ready[s] = j + 1;
+    }
+  }
+}
+
+// Variant 3: as variant 2, but the chain of adds runs in one thread with
+// the limbs in registers (longfloat.cuh lf::add<N>: select-based shifters,
+// no cross-lane steps), the products still formed by the warp-cooperative
+// multiply; the ring carries them as lf::DF.
+template <int N>
+__global__ void __launch_bounds__(32 * (1 + LR_PROD))
+long_residual_split1_kernel(const lf::DF *__restrict__ A,
+                            const lf::DF *__restrict__ x,
+                            const lf::DF *__restrict__ b,
+                            lf::DF *__restrict__ res, int n, int p) {
+  __shared__ uint64_t ring_m[LR_RING][N];
+  __shared__ int64_t ring_e[LR_RING];
+  __shared__ int ring_s[LR_RING];
+  __shared__ volatile int ready[LR_RING];
+  __shared__ volatile int consumed;
+  const int row = blockIdx.x, warp = threadIdx.x >> 5, t = threadIdx.x & 31;
+  if (threadIdx.x < LR_RING) ready[threadIdx.x] = 0;
+  if (threadIdx.x == 0) consumed = 0;
+  __syncthreads();
+  const lf::DF *arow = A + (int64_t)row * n;
+  if (warp == 0) {
+    if (t != 0) return;
+    lf::DF acc = lf::zero();
+    for (int j = 0; j < n; ++j) {
+      const int s = j % LR_RING;
+      while (ready[s] != j + 1) {
+      }
+      __threadfence_block();
+      lf::DF pr = lf::zero();
+      pr.sign = ring_s[s];
+      pr.exp = ring_e[s];
+#pragma unroll
+      for (int i = 0; i < N; ++i) pr.m[i] = ring_m[s][i];
+      __threadfence_block();
+      consumed = j + 1;
+      acc = lf::add<N>(acc, pr, p);
+    }
+    res[row] = lf::add<N>(b[row], lf::neg(acc), p);
+    if (res[row].sign == 0) res[row].exp = 0;
+  } else {
+    auto load = [&](const lf::DF &v) {
+      lw::WV w;
+      w.m = t < lf::NL ? v.m[t] : 0ull;
+      w.exp = v.exp;
+      w.sign = v.sign;
+      return w;
+    };
+    const int pw = warp - 1;
+    int j = pw;
+    lw::WV an, xn;
+    if (j < n) {
+      an = load(arow[j]);
+      xn = load(x[j]);
+    }
+    for (; j < n; j += LR_PROD) {
+      const lw::WV aj = an, xj = xn;
+      if (j + LR_PROD < n) {
+        an = load(arow[j + LR_PROD]);
+        xn = load(x[j + LR_PROD]);
+      }
+      const lw::WV pr = lw::mul(aj, xj, p);
+      const int s = j % LR_RING;
+      while (lw::uni(consumed <= j - LR_RING)) __nanosleep(64);
+      __threadfence_block();
+      if (t < N) ring_m[s][t] = pr.m;
+      if (t == 0) {
+        ring_e[s] = pr.exp;
+        ring_s[s] = pr.sign;
+      }
+      __threadfence_block();
+      __syncwarp();
+      if (t == 0) ready[s] = j + 1;
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t long_residual(int p, int n, const void *A, const void *x,
                           const void *b, void *res, cudaStream_t s,
                           int variant) {
   if (n <= 0) return cudaSuccess;
+  if (variant == 3 && p <= 512) {
+    auto a3 = static_cast<const lf::DF *>(A);
+    auto x3 = static_cast<const lf::DF *>(x);
+    auto b3 = static_cast<const lf::DF *>(b);
+    auto r3 = static_cast<lf::DF *>(res);
+    switch ((p + 63) >> 6) {
+#define LR3_CASE(NN)                                                        \
+  case NN:                                                                  \
+    long_residual_split1_kernel<NN><<<n, 32 * (1 + LR_PROD), 0, s>>>(      \
+        a3, x3, b3, r3, n, p);                                              \
+    break;
+      LR3_CASE(1) LR3_CASE(2) LR3_CASE(3) LR3_CASE(4)
+      LR3_CASE(5) LR3_CASE(6) LR3_CASE(7) LR3_CASE(8)
+#undef LR3_CASE
+    }
+    return cudaGetLastError();
+  }
+  if (variant == 2 && p <= 512) {
+    long_residual_split_kernel<<<n, 32 * (1 + LR_PROD), 0, s>>>(
+        static_cast<const lf::DF *>(A), static_cast<const lf::DF *>(x),
+        static_cast<const lf::DF *>(b), static_cast<lf::DF *>(res), n, p);
+    return cudaGetLastError();
+  }
   if (variant == 0 && p <= 512) {
     long_residual_warp_kernel<<<(n + 3) / 4, 128, 0, s>>>(
         static_cast<const lf::DF *>(A), static_cast<const lf::DF *>(x),

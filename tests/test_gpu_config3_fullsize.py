@@ -5,8 +5,11 @@ n = 1024, kappa = 1e30, 512-bit system written by mpcore_write_config3
 CPU time).  The native driver must reproduce the iteration count, the stop
 reason, the residual history (40 digits) and the solution (60 digits,
 SHA-256 of the text) exactly -- with the ||A||_F-bounds shortcut and with
-the exact norm, and with the one-call factor_solve and with factor() then
-solve() -- both in memory and through the .mpmat files."""
+the exact norm, with the one-call factor_solve (asynchronous, overlapping
+the host conversion, or not) and with factor() then solve() -- both in
+memory and through the .mpmat files.  (MPCORE_RESIDUAL_VARIANT is read once
+per process, so the warp-per-row residual variant is pinned by
+tests/test_gpu_long_residual.py instead.)"""
 
 import ctypes
 import hashlib
@@ -42,12 +45,17 @@ def check(rep):
         G["solution_sha"]
 
 
-@pytest.mark.parametrize("mode", ["bounds", "exact_fro", "split_factor"])
+@pytest.mark.parametrize("mode", ["bounds", "exact_fro", "split_factor",
+                                  "no_overlap"])
 def test_config3_n1024_matches_reference(mode, monkeypatch):
+    # bounds: the production path (asynchronous factorisation overlapping
+    # the fixed-width conversion, products-off-the-chain residual)
     if mode == "exact_fro":
         monkeypatch.setenv("MPCORE_REFINE_EXACT_FRO", "1")
     if mode == "split_factor":
         monkeypatch.setenv("MPCORE_REFINE_SPLIT_FACTOR", "1")
+    if mode == "no_overlap":
+        monkeypatch.setenv("MPCORE_REFINE_NO_OVERLAP", "1")
     h = ctypes.c_uint64()
     assert nat.lib().mpcore_refine_config3(
         G["n"], G["seed"], G["kappa_exp10"], 3, 512, b"1e-100", b"0", 20, 0,

@@ -11,11 +11,12 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 @pytest.mark.parametrize("prec", [53, 64, 65, 106, 200, 300, 424, 511, 512])
 @pytest.mark.parametrize("n", [1, 7, 33])
 def test_device_residual_matches_host(prec, n, variant):
-    # variant 0: warp per row (production), 1: thread per row
+    # variant 2: products off the chain (production), 0: warp per row,
+    # 1: thread per row
     from paper_2107_12550_b200 import _native as nat
     m = ctypes.c_int64(-1)
     nat.check(nat.lib().mpcore_debug_long_residual_selftest(
@@ -24,9 +25,10 @@ def test_device_residual_matches_host(prec, n, variant):
     assert m.value == 0
 
 
-def test_device_residual_larger():
+@pytest.mark.parametrize("variant", [0, 2, 3])
+def test_device_residual_larger(variant):
     from paper_2107_12550_b200 import _native as nat
     m = ctypes.c_int64(-1)
     nat.check(nat.lib().mpcore_debug_long_residual_selftest(
-        256, 512, 99, 0, ctypes.byref(m)), "residual selftest")
+        256, 512, 99, variant, ctypes.byref(m)), "residual selftest")
     assert m.value == 0
