@@ -640,7 +640,11 @@ def run_dist(args):
         torch.cuda.synchronize()
     ms = max_over_ranks(pg, ev0.elapsed_time(ev1) / args.steps)
     # per-panel critical-path breakdown: one more step with phase events
+    # (--dist-trace PATH: every phase of every panel, start / end ms)
+    if args.dist_trace and rank == 0:
+        os.environ["MPCORE_DIST_TRACE"] = args.dist_trace
     _, phases, _ = step(phases=True)
+    os.environ.pop("MPCORE_DIST_TRACE", None)
     torch.cuda.synchronize()
     xs = x.cpu().numpy()
     # end to end: this rank's columns from page-locked host memory each
@@ -943,6 +947,8 @@ def main():
                     help="CPU baseline sample size (0: per config)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-trace", default="",
+                    help="config 4: write the per-panel phase timeline here")
     args = ap.parse_args()
     if args.config is None:
         multi = int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.gpus > 1

@@ -469,9 +469,15 @@ cudaError_t ensure_rank(RankWork &r, int k, int n, int nb) {
 // phase timing (optional): event pairs per phase, summed at the end
 struct Phases {
   bool on = false;
+  int panel = -1;  // the panel the next records belong to
   std::vector<cudaEvent_t> pool;
-  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> recs;
+  struct Rec {
+    int ph, panel;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
   cudaEvent_t open_a[DIST_NPHASES] = {};
+  int open_p[DIST_NPHASES] = {};
   cudaEvent_t mk() {
     cudaEvent_t e;
     cudaEventCreate(&e);
@@ -481,24 +487,38 @@ struct Phases {
   void begin(int ph, cudaStream_t s) {
     if (!on) return;
     open_a[ph] = mk();
+    open_p[ph] = panel;
     cudaEventRecord(open_a[ph], s);
   }
   void end(int ph, cudaStream_t s) {
     if (!on || !open_a[ph]) return;
     cudaEvent_t b = mk();
     cudaEventRecord(b, s);
-    recs.push_back({ph, {open_a[ph], b}});
+    recs.push_back({ph, open_p[ph], open_a[ph], b});
     open_a[ph] = nullptr;
   }
+  // sums per phase; with MPCORE_DIST_TRACE=path also every record as
+  // "phase panel start_ms end_ms" relative to the call's first event
   void collect(double *ms) {
+    static const char *names[DIST_NPHASES] = {"total", "factor", "bcast",
+                                              "exch_trsm", "update", "back"};
     for (int i = 0; i < DIST_NPHASES; ++i) ms[i] = 0;
+    const char *path = std::getenv("MPCORE_DIST_TRACE");
+    FILE *f = path ? std::fopen(path, "w") : nullptr;
+    if (f) std::fprintf(f, "phase panel start_ms end_ms\n");
+    cudaEvent_t origin = recs.empty() ? nullptr : recs.front().a;
+    for (auto &r : recs)
+      if (r.ph == DIST_TOTAL) origin = r.a;
     for (auto &r : recs) {
-      float t = 0;
-      if (cudaEventSynchronize(r.second.second) == cudaSuccess &&
-          cudaEventElapsedTime(&t, r.second.first, r.second.second) ==
-              cudaSuccess)
-        ms[r.first] += t;
+      float t = 0, t0 = 0, t1 = 0;
+      if (cudaEventSynchronize(r.b) == cudaSuccess &&
+          cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess)
+        ms[r.ph] += t;
+      if (f && origin && cudaEventElapsedTime(&t0, origin, r.a) == cudaSuccess &&
+          cudaEventElapsedTime(&t1, origin, r.b) == cudaSuccess)
+        std::fprintf(f, "%s %d %.4f %.4f\n", names[r.ph], r.panel, t0, t1);
     }
+    if (f) std::fclose(f);
   }
   ~Phases() {
     for (auto e : pool) cudaEventDestroy(e);
@@ -611,6 +631,7 @@ int dist_lu_solve(void *comm, int k, int n, int nb, int G,
         (e = cudaStreamWaitEvent(S2, rw.ev_blk, 0)) ||
         (e = cudaStreamWaitEvent(S2, rw.ev_consumed[s], 0)))
       return fail(e, "factor order");
+    ph.panel = P;
     ph.begin(DIST_FACTOR, S2);
     MatView blk = at(V.A, J, off);
     if ((e = lu_factor_async(k, n - J, w, blk, rw.tswaps, 32, ws, S2)))
@@ -640,6 +661,7 @@ int dist_lu_solve(void *comm, int k, int n, int nb, int G,
         return fail(e, "slot reuse");
       bufs[i] = rw.slot[s];
       streams[i] = rw.C;
+      ph.panel = P;
       ph.begin(DIST_BCAST, rw.C);
     }
     const int root_idx = comm ? 0 : idx_of[root];
@@ -663,6 +685,7 @@ int dist_lu_solve(void *comm, int k, int n, int nb, int G,
     const int J = P * nb, w = width(P), s = P % 2;
     const double *pl = slot_planes(rw, s);
     MatView Ls{const_cast<double *>(pl), w, (int64_t)(n - J) * w};
+    ph.panel = P;
     ph.begin(DIST_EXCH_TRSM, rw.S);
     for (auto &r : ex) {
       if (r.second <= 0) continue;
@@ -758,6 +781,7 @@ int dist_lu_solve(void *comm, int k, int n, int nb, int G,
   // ---- back substitution, column-cyclic, blocks last to first ----
   for (int i = 0; i < R; ++i) {
     RankWork &rw = *DW.ranks[i];
+    ph.panel = -1;
     ph.begin(DIST_BACK, rw.S);
     const DistRankView &V = views[i];
     if ((e = copy2d(k, n, 1, rw.v, 1, n, V.A.p + lc[i], V.A.ld, V.A.plane,

@@ -367,19 +367,29 @@ class NcclComm:
     group (any backend; one small object broadcast at setup)."""
 
     def __init__(self, world, rank, group=None):
-        import torch.distributed as dist
-        L = nat.lib()
+        uid = self.exchange_id(world, rank, group)
+        h = nat._u64()
+        nat.check(nat.lib().mpcore_dist_comm_init(world, rank, uid, 128,
+                                                  ctypes.byref(h)),
+                  "dist_comm_init")
+        self.handle, self.world, self.rank = h.value, world, rank
+
+    @staticmethod
+    def exchange_id(world, rank, group=None):
+        """Rank 0 draws the 128-byte NCCL unique id (mpcore_dist_unique_id)
+        and every rank receives it over the torch.distributed group; ->
+        bytes."""
         obj = [None]
         if rank == 0:
             buf = ctypes.create_string_buffer(128)
-            nat.check(L.mpcore_dist_unique_id(buf, 128), "dist_unique_id")
+            nat.check(nat.lib().mpcore_dist_unique_id(buf, 128),
+                      "dist_unique_id")
             obj[0] = buf.raw
         if world > 1:
+            import torch.distributed as dist
             dist.broadcast_object_list(obj, src=0, group=group)
-        h = nat._u64()
-        nat.check(L.mpcore_dist_comm_init(world, rank, obj[0], 128,
-                                          ctypes.byref(h)), "dist_comm_init")
-        self.handle, self.world, self.rank = h.value, world, rank
+        assert isinstance(obj[0], bytes) and len(obj[0]) == 128
+        return obj[0]
 
     def close(self):
         if self.handle:

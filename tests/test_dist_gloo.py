@@ -198,3 +198,44 @@ def test_gloo_world_matches_reference_lu(tmp_path, k, n, nb, world, lookahead):
         full[:, :, layout.global_columns(r)] = np.load(tmp_path / ("rank%d.npy" % r))
         assert np.load(tmp_path / ("swaps%d.npy" % r)).tobytes() == sw_ref.tobytes()
     assert full.tobytes() == lu_ref.tobytes()
+
+
+def _id_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    from paper_2107_12550_b200 import _native as nat
+    from paper_2107_12550_b200.dist import NcclComm
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        uid = NcclComm.exchange_id(world, rank)
+        with open(os.path.join(out_dir, "id%d" % rank), "wb") as fh:
+            fh.write(uid)
+        # no GPU here: creating the communicator must fail loudly (status
+        # 6 with the library's message), never fall back
+        try:
+            NcclComm(world, rank)
+            ok = "created"
+        except nat.NativeError as e:
+            ok = "refused %d" % e.status
+        with open(os.path.join(out_dir, "init%d" % rank), "w") as fh:
+            fh.write(ok)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_bootstrap_id_over_gloo(tmp_path):
+    # the native distributed driver's bootstrap at world size 2: one NCCL
+    # unique id drawn on rank 0 (libnccl via dlopen), identical on every rank
+    import torch.multiprocessing as mp
+    from paper_2107_12550_b200 import _native as nat
+    if torch.cuda.is_available():
+        pytest.skip("CPU-only check (the GPU suite covers the communicator)")
+    mp.spawn(_id_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2,
+             join=True)
+    ids = [open(tmp_path / ("id%d" % r), "rb").read() for r in range(2)]
+    assert len(ids[0]) == 128 and ids[0] == ids[1] and any(ids[0])
+    for r in range(2):
+        assert open(tmp_path / ("init%d" % r)).read() == \
+            "refused %d" % nat.INTERNAL
