@@ -444,6 +444,14 @@ def run_ours(args):
             api_t.append(time.perf_counter() - t0)
     assert xs_api.data.tobytes() == x.download().tobytes()
     api_ms = max_over_ranks(pg, statistics.median(api_t) * 1e3)
+    bwd = None
+    if rank == 0 and k < 4:
+        import torch
+        dev = torch.device("cuda", local)
+        bwd = qd_backward_error(
+            k, n, torch.from_numpy(A0.download()).to(dev),
+            torch.from_numpy(b.download()).to(dev),
+            torch.from_numpy(x.download()).to(dev))
     if rank != 0:
         return
     flops = (2.0 / 3.0) * n ** 3
@@ -482,6 +490,7 @@ def run_ours(args):
                         "substitution; = lu_factor + lu_solve bit for bit) + "
                         "get_planes(x); K uploads, K solves, K downloads "
                         "between the events"},
+        "check": bwd,
         "api_e2e": {"value": world * flops / (api_ms * 1e-3) / 1e9,
                     "unit": "GFLOP/s", "ms_per_step": api_ms,
                     "h2d_bytes_per_step": (2 * k * n * n + k * n) * 8,
@@ -541,6 +550,46 @@ def traffic_bytes(k, n):
     except (OSError, ValueError):
         return None
     return d["dram_bytes"] if (d.get("k"), d.get("n")) == (k, n) else None
+
+
+U_P = {2: 2.0 ** -104, 3: 2.0 ** -156, 4: 2.0 ** -208}
+
+
+def qd_backward_error(k, n, A, b, x):
+    """Normwise backward error ||b - A x||_inf / (||A||_inf ||x||_inf) with
+    the residual formed in QD on the GPU (k-component inputs lift to QD
+    exactly; mat_vec and the subtraction are the library's kernels).  A: a
+    CUDA tensor (k, n, ld >= n), b and x: (k, n).  The north star's bound
+    is n * u_p (DD 2^-104, TD 2^-156)."""
+    import torch
+    from paper_2107_12550_b200 import _native as nat
+    from paper_2107_12550_b200.linalg import DeviceVector
+    ld = A.shape[2]
+    Aq = torch.zeros((4, n, ld), dtype=torch.float64, device=A.device)
+    Aq[:k] = A
+    xq = torch.zeros((4, n), dtype=torch.float64, device=A.device)
+    xq[:k] = x
+    y = torch.zeros_like(xq)
+    torch.cuda.synchronize()
+    nat.check(nat.lib().mpcore_dev_matvec(4, n, n, Aq.data_ptr(), ld, n * ld,
+                                          xq.data_ptr(), y.data_ptr()),
+              "QD mat_vec")
+    bq = torch.zeros_like(xq)
+    bq[:k] = b
+    B = DeviceVector.from_planes(bq.cpu().numpy())
+    Y = DeviceVector.from_planes((-y).cpu().numpy())
+    R = DeviceVector(4, n)
+    nat.check(nat.lib().mpcore_elementwise(0, B.handle, Y.handle, R.handle),
+              "QD subtract")
+    r = float(np.max(np.abs(R.download()[0])))
+    norm_a = float(A[0, :, :n].abs().sum(dim=1).max())
+    norm_x = float(x[0].abs().max())
+    del Aq
+    torch.cuda.empty_cache()
+    return {"backward_error": r / (norm_a * norm_x),
+            "bound_n_u": n * U_P[k],
+            "residual": "b - A x in QD on the GPU (mat_vec + subtraction "
+                        "kernels), norms from the heads"}
 
 
 def config4_work(n, nb):
@@ -613,7 +662,8 @@ def run_dist(args):
     M = M0.clone()
     torch.cuda.synchronize()
     x = torch.zeros((k, n), dtype=torch.float64, device=M.device)
-    comm = NcclComm(world, rank)
+    with stdout_to_stderr():      # (NCCL's version banner goes to stdout)
+        comm = NcclComm(world, rank)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
 
@@ -687,6 +737,8 @@ def run_dist(args):
             pg.barrier()
         return
     err = float(np.max(np.abs((xs[0] - 1.0) + xs[1])))
+    bwd = qd_backward_error(k, n, M0, M0[:, :, lc], x) if world == 1 \
+        else None
     flops = (2.0 / 3.0) * n ** 3
     wc = work_counts(n, k)
     upd_instr = config4_work(n, nb) * MADD_INSTR[k]
@@ -704,7 +756,7 @@ def run_dist(args):
         "dtype": "f64x%d (%s, bit-exact EFT arithmetic)" % (k, NAMES[k]),
         "data": "synthetic (seeded recipe, SURVEY 8d; seed %d)" % seed,
         "config": config_dict(args, world),
-        "check": {"max_abs_err_x_vs_ones": err},
+        "check": {"max_abs_err_x_vs_ones": err, **(bwd or {})},
         "roofline": {
             "bound": "fp64",
             "kernel": "trailing update (gemm_kernel NEG_A, K = %d), rank 0"

@@ -120,3 +120,66 @@ def test_native_singular_step(G):
     with pytest.raises(SingularMatrixError) as ei:
         dist_lu_solve(layout, local, xs, k)
     assert ei.value.step == 70
+
+
+@pytest.mark.parametrize("k,n,G", [(2, 2048, 2), (2, 4096, 4), (3, 2048, 3)])
+def test_native_config4_path_vs_oracle(k, n, G):
+    # SURVEY §8(c) config-4 plan, step 1: the nb = 256 column-cyclic path
+    # byte-compared with the oracle at n = 2048 / 4096
+    layout, local, xs, A, b = build(k, n, 256, G, 210712554 + n)
+    swaps, _, _ = dist_lu_solve(layout, local, xs, k)
+    lu_ref, sw_ref = oracle.lu(A)
+    assert swaps.tobytes() == sw_ref.tobytes()
+    for r in range(G):
+        cols = layout.global_columns(r)
+        assert local[r].cpu().numpy()[:, :, :len(cols)].tobytes() == \
+            np.ascontiguousarray(lu_ref[:, :, cols]).tobytes()
+    assert xs[0].cpu().numpy().tobytes() == \
+        oracle.solve(lu_ref, sw_ref, b).tobytes()
+
+
+def test_native_rank_invariance_n16384():
+    # step 2 of the plan at n = 16384 (DD, 4.3 GB): G = 1, 4 and 8 virtual
+    # ranks give the same pivots, factors and x bit for bit
+    k, n, nb = 2, 16384, 256
+    seed = 210712554
+    ref = None
+    for G in (1, 4, 8):
+        layout = Layout(n, nb, G)
+        be = DeviceBackend(k)
+        full = be.alloc(n, n)
+        be.generate(full, Layout(n, nb, 1), 0, 0, seed)
+        xt = torch.zeros((k, n), dtype=torch.float64, device="cuda")
+        xt[0] = 1.0
+        bb = torch.zeros_like(xt)
+        torch.cuda.synchronize()
+        nat.check(nat.lib().mpcore_dev_matvec(k, n, n, full.data_ptr(), n,
+                                              n * n, xt.data_ptr(),
+                                              bb.data_ptr()), "mv")
+        local, xs = {}, {}
+        for r in range(G):
+            cols = torch.as_tensor(layout.global_columns(r), device="cuda")
+            M = torch.empty((k, n, len(cols) + 1), dtype=torch.float64,
+                            device="cuda")
+            M[:, :, :len(cols)] = full[:, :, cols]
+            M[:, :, len(cols)] = bb
+            local[r] = M
+            xs[r] = torch.zeros_like(xt)
+        del full
+        torch.cuda.synchronize()
+        swaps, _, _ = dist_lu_solve(layout, local, xs, k)
+        # factors back in global column order, compared bitwise on the GPU
+        fact = torch.empty((k, n, n), dtype=torch.float64, device="cuda")
+        for r in range(G):
+            cols = torch.as_tensor(layout.global_columns(r), device="cuda")
+            fact[:, :, cols] = local[r][:, :, :-1]
+        res = (swaps.tobytes(), xs[0].cpu().numpy().tobytes())
+        if ref is None:
+            ref, ref_fact = res, fact
+        else:
+            assert res == ref
+            assert torch.equal(fact.view(torch.int64),
+                               ref_fact.view(torch.int64))
+            del fact
+        del local, xs
+        torch.cuda.empty_cache()
