@@ -277,6 +277,12 @@ int32_t mpcore_dist_lu_solve(uint64_t comm, int32_t k, int32_t n, int32_t nb,
  * with 0xA5; this checks every live guarded object: *checked of them,
  * *bad with a written zone */
 int32_t mpcore_debug_check_guards(int64_t *checked, int64_t *bad);
+/* selftest: the GPU long -> short conversion of the refinement driver
+ * (round to prec bits, k binary64 heads) against the host's on iters
+ * random values; *mismatches = values differing in any bit */
+int32_t mpcore_debug_convert_selftest(int64_t iters, uint64_t seed,
+                                      int32_t prec, int32_t k,
+                                      int64_t *mismatches);
 
 /* select the CUDA device for this process (before any other call) */
 int32_t mpcore_set_device(int32_t device);

@@ -116,6 +116,8 @@ _PROTOS = {
                                           _u64]),
     "mpcore_debug_check_guards": (_i32, [ctypes.POINTER(_i64),
                                          ctypes.POINTER(_i64)]),
+    "mpcore_debug_convert_selftest": (_i32, [_i64, _u64, _i32, _i32,
+                                             ctypes.POINTER(_i64)]),
     # the native distributed LU + solve (dist.cu; BASELINE config 4)
     "mpcore_dist_unique_id": (_i32, [ctypes.c_char_p, _i32]),
     "mpcore_dist_comm_init": (_i32, [_i32, _i32, ctypes.c_char_p, _i32,

@@ -684,6 +684,10 @@ struct IrWorkspace {
   // page-locked results of an asynchronous factor_solve: status, swaps, x
   void *hres_fs = nullptr;
   size_t hres_fscap = 0;
+  // the device conversion's scratch: bad flag, max exponent, partial sums
+  // (device) and their page-locked copies
+  void *dconv = nullptr, *hconv = nullptr;
+  size_t dconvcap = 0, hconvcap = 0;
   cudaStream_t up = nullptr;
   cudaEvent_t up_done = nullptr;
 };
@@ -866,9 +870,12 @@ class GpuShortSolver : public mpr::ShortSolver {
         D.swaps_cap = n;
     }
     for (int c = 0; c < k && e == cudaSuccess; ++c) {
-      e = cudaMemcpy2DAsync(a_ + c * plane, (n + 1) * 8, a + (size_t)c * n * n,
-                            (size_t)n * 8, (size_t)n * 8, n,
-                            cudaMemcpyHostToDevice, D.stream);
+      // (A's planes are already in place when the device converted them)
+      if (!a_on_device_)
+        e = cudaMemcpy2DAsync(a_ + c * plane, (n + 1) * 8,
+                              a + (size_t)c * n * n, (size_t)n * 8,
+                              (size_t)n * 8, n, cudaMemcpyHostToDevice,
+                              D.stream);
       if (e == cudaSuccess)
         e = cudaMemcpy2DAsync(a_ + c * plane + n, (n + 1) * 8,
                               b.data() + (size_t)c * n, 8, 8, n,
@@ -937,6 +944,109 @@ class GpuShortSolver : public mpr::ShortSolver {
     }
     return MPCORE_OK;
   }
+  // ---- the long -> short conversion on the device (convert.cu) ----
+  bool device_convert_supported(int p) override {
+    return p <= 512 && claim();
+  }
+  int device_convert_begin(int k, int n, int p, const void *flat,
+                           std::string &err) override {
+    if (!claim()) { err = "no conversion workspace"; return MPCORE_INTERNAL; }
+    DevLock L;
+    if (L.st) { err = g_err; return L.st; }
+    Device &D = device();
+    IrWorkspace &w = ir_ws();
+    if (flat != w.stage) { err = "flat input must be staging slot 0"; return MPCORE_INTERNAL; }
+    const size_t nn = (size_t)n * n, plane = (size_t)n * (n + 1);
+    const size_t sc = 16 + (size_t)mpk::long_to_short_partials() * sizeof(double);
+    cudaError_t e = ensure_buffers((size_t)k * plane * sizeof(double),
+                                   (size_t)k * n * 8, (size_t)n * 4);
+    if (e == cudaSuccess) e = grow_dev(&w.rA, w.rAcap, nn * LF_BYTES);
+    if (e == cudaSuccess) e = grow_dev(&w.dconv, w.dconvcap, sc);
+    if (e == cudaSuccess) e = grow_host(&w.hconv, w.hconvcap, sc);
+    char *dc = static_cast<char *>(w.dconv);
+    if (e == cudaSuccess)
+      e = mpk::long_to_short_init(reinterpret_cast<int *>(dc),
+                                  reinterpret_cast<int *>(dc + 4), D.stream);
+    if (e != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
+    ck_ = k;
+    cn_ = n;
+    cp_ = p;
+    return MPCORE_OK;
+  }
+  int device_convert_rows(int r0, int r1, std::string &err) override {
+    DevLock L;
+    if (L.st) { err = g_err; return L.st; }
+    Device &D = device();
+    IrWorkspace &w = ir_ws();
+    const int n = cn_;
+    const size_t plane = (size_t)n * (n + 1);
+    char *dc = static_cast<char *>(w.dconv);
+    const size_t off = (size_t)r0 * n * LF_BYTES;
+    cudaError_t e = cudaMemcpyAsync(static_cast<char *>(w.rA) + off,
+                                    static_cast<char *>(w.stage) + off,
+                                    (size_t)(r1 - r0) * n * LF_BYTES,
+                                    cudaMemcpyHostToDevice, D.stream);
+    if (e == cudaSuccess)
+      e = mpk::long_to_short_rows(ck_, n, cp_, w.rA, r0, r1, a_, n + 1,
+                                  (int64_t)plane, reinterpret_cast<int *>(dc),
+                                  reinterpret_cast<int *>(dc + 4), D.stream);
+    if (e != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
+    return MPCORE_OK;
+  }
+  int device_convert_end(int *emax, double *hsum, std::string &err) override {
+    DevLock L;
+    if (L.st) { err = g_err; return L.st; }
+    Device &D = device();
+    IrWorkspace &w = ir_ws();
+    const int np = mpk::long_to_short_partials();
+    const size_t sc = 16 + (size_t)np * sizeof(double);
+    char *dc = static_cast<char *>(w.dconv), *hc = static_cast<char *>(w.hconv);
+    cudaError_t e = mpk::long_to_short_stats(
+        cn_, a_, cn_ + 1, reinterpret_cast<const int *>(dc + 4),
+        reinterpret_cast<double *>(dc + 16), D.stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(hc, dc, sc, cudaMemcpyDeviceToHost, D.stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(D.stream);
+    if (e != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
+    int bad;
+    std::memcpy(&bad, hc, 4);
+    std::memcpy(emax, hc + 4, 4);
+    double s = 0.0;
+    for (int i = 0; i < np; ++i) {
+      double v;
+      std::memcpy(&v, hc + 16 + (size_t)i * sizeof(double), sizeof v);
+      s += v;
+    }
+    *hsum = s;
+    if (bad) return MPCORE_OVERFLOW;  // a head outside binary64: host path
+    rn_ = cn_;
+    a_on_device_ = true;
+    af_on_device_ = true;
+    return MPCORE_OK;
+  }
+  int download_long_A(void *dst, std::string &err) override {
+    if (!af_on_device_) { err = "no device copy of A"; return MPCORE_INTERNAL; }
+    DevLock L;
+    if (L.st) { err = g_err; return L.st; }
+    IrWorkspace &w = ir_ws();
+    cudaError_t e = cudaMemcpyAsync(dst, w.rA, (size_t)rn_ * rn_ * LF_BYTES,
+                                    cudaMemcpyDeviceToHost, device().stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(device().stream);
+    if (e != cudaSuccess) {
+      err = cudaGetErrorString(e);
+      return MPCORE_INTERNAL;
+    }
+    return MPCORE_OK;
+  }
   // ---- the long residual on the device (residual.cu) ----
   bool residual_supported(int p) override { return p <= 512 && claim(); }
   void *staging(int slot, size_t bytes) override {
@@ -992,8 +1102,9 @@ class GpuShortSolver : public mpr::ShortSolver {
     upload_pending_ = false;
     IrWorkspace &w = ir_ws();
     const size_t mb = (size_t)rn_ * rn_ * LF_BYTES, vb = (size_t)rn_ * LF_BYTES;
-    cudaError_t e = cudaMemcpyAsync(w.rA, w.stage, mb, cudaMemcpyHostToDevice,
-                                    w.up);
+    cudaError_t e = cudaSuccess;
+    if (!af_on_device_)  // (else the device conversion wrote it)
+      e = cudaMemcpyAsync(w.rA, w.stage, mb, cudaMemcpyHostToDevice, w.up);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(w.rb, w.hx, vb, cudaMemcpyHostToDevice, w.up);
     if (e == cudaSuccess) e = cudaEventRecord(w.up_done, w.up);
@@ -1093,6 +1204,9 @@ class GpuShortSolver : public mpr::ShortSolver {
   int ld_ = 0;  // row stride of the factors (n, or n + 1 after factor_solve)
   bool upload_pending_ = false;
   bool inflight_ = false;  // factor_solve_begin without its end yet
+  int ck_ = 0, cn_ = 0, cp_ = 0;  // the conversion in flight
+  bool a_on_device_ = false;   // device_convert filled a_'s A planes
+  bool af_on_device_ = false;  // ... and the rounded long A (w.rA)
   bool tried_ = false;
   bool shared_ = false;  // buffers borrowed from ir_ws()
   double *a_ = nullptr, *b_ = nullptr, *x_ = nullptr;
@@ -2158,6 +2272,20 @@ int32_t mpcore_debug_check_guards(int64_t *checked, int64_t *bad) {
       }
   }
   return MPCORE_OK;
+}
+
+
+// the device long -> short conversion (convert.cu) against the host's
+// fixed-width from_bf + to_multicomp: mismatching values over iters
+int32_t mpcore_debug_convert_selftest(int64_t iters, uint64_t seed,
+                                      int32_t prec, int32_t k,
+                                      int64_t *mismatches) {
+  if (!mismatches) return MPCORE_BAD_DIMENSION;
+  DevLock L;
+  if (L.st) return L.st;
+  *mismatches = mpr::convert_selftest(iters, seed, prec, k, device().stream);
+  return *mismatches < 0 ? fail(MPCORE_BAD_DIMENSION, "bad selftest arguments")
+                         : MPCORE_OK;
 }
 
 }  // extern "C"

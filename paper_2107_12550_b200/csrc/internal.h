@@ -62,6 +62,22 @@ int num_sms();
 cudaError_t long_residual(int p, int n, const void *A, const void *x,
                           const void *b, void *res, cudaStream_t s,
                           int variant = 0);
+// the IR's long -> short conversion (convert.cu), in row chunks: A (n x n
+// lf::DF; rows [r0, r1) flat exact values in, rounded to p out, in place),
+// their k heads into the planes (ld, plane), *d_bad when a head leaves the
+// binary64 range and the largest head exponent (*d_emax); then the
+// long_to_short_partials() per-block sums of the heads' squares scaled by
+// 2^-emax
+cudaError_t long_to_short_init(int *d_bad, int *d_emax, cudaStream_t s);
+cudaError_t long_to_short_rows(int k, int n, int p, void *A, int r0, int r1,
+                               double *planes, int64_t ld, int64_t plane,
+                               int *d_bad, int *d_emax, cudaStream_t s);
+cudaError_t long_to_short_stats(int n, const double *planes, int64_t ld,
+                                const int *d_emax, double *d_partials,
+                                cudaStream_t s);
+int long_to_short_partials();
+cudaError_t long_to_short_selftest(int k, int p, void *A, int64_t count,
+                                   double *heads, int *ok, cudaStream_t s);
 // diagnostics: per-panel kernel stamps into buf ([4 * n] u64) or off (null)
 cudaError_t lu_stamps_enable(unsigned long long *buf);
 

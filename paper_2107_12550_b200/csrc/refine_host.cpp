@@ -352,6 +352,19 @@ struct PhaseLog {
   }
 };
 
+// exact value of v into the flat fixed-width form the device conversion
+// reads (ff::F layout, limbs not normalised); false when wider than NL limbs
+static bool flat_from_bf(const BF &v, ff::F &f) {
+  f.sign = v.sign;
+  f.exp = v.exp;
+  const size_t n32 = v.man.w.size();
+  if (n32 > 2 * (size_t)ff::NL) return false;
+  std::memset(f.m, 0, sizeof f.m);
+  if (n32) std::memcpy(f.m, v.man.w.data(), n32 * sizeof(uint32_t));
+  if (v.sign == 0) f.exp = 0;
+  return true;
+}
+
 // software prefetch of a value's heap-allocated mantissa limbs
 constexpr size_t kPrefetch = 24;
 static inline void prefetch_bf(const BF &v) {
@@ -426,7 +439,13 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
   BF a_fro;
   const int T = (int)std::max<size_t>(1, std::min<size_t>((size_t)threads, nn));
   bool fro_exact = !fast;     // a_fro holds the exact ||A||_F
+  bool af_on_host = true;  // Af holds the rounded A (else the flat input)
   auto exact_fro = [&]() {
+    if (!af_on_host) {  // the rounded A lives on the device
+      std::string e2;
+      if (S.download_long_A(Af.p, e2)) return false;
+      af_on_host = true;
+    }
     RawBuf<ff::F> sq;  // squares on all threads, summed in order
     if (!sq.alloc(nn)) return false;
     par_rows(nn, threads, [&](size_t a, size_t b) {
@@ -446,7 +465,87 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
   const bool split_factor = std::getenv("MPCORE_REFINE_SPLIT_FACTOR") != nullptr;
   const bool overlap = fast && dev_res && !split_factor &&
                        std::getenv("MPCORE_REFINE_NO_OVERLAP") == nullptr;
-  if (fast) {
+  // the conversion on the GPU: the host only lays the
+  // exact values out flat in the staging buffer (one copy of each
+  // mantissa), the device rounds them to p, keeps them for the residual and
+  // peels the heads straight into the factorisation's workspace
+  bool dev_conv = overlap && S.device_convert_supported(pi) &&
+                  std::getenv("MPCORE_REFINE_HOST_CONVERT") == nullptr;
+  if (dev_conv) {
+    // row chunks: the host flattens chunk c + 1 while chunk c uploads and
+    // converts
+    std::atomic<bool> wide{false};
+    bool ok = true;
+    st = S.device_convert_begin(k, n, pi, Af.p, err);
+    if (st) return st;
+    const int chunks = std::max(1, std::min(8, n / 64));
+    // every thread flattens its share of each chunk in turn; thread 0 then
+    // waits for the chunk's other shares and hands it to the device, while
+    // the others already work on the next chunk
+    std::vector<std::atomic<int>> done(chunks);
+    for (auto &d : done) d.store(0);
+    std::atomic<int> dev_st{0};
+    std::string dev_err;
+    auto chunk_rows = [&](int c, int &r0, int &r1) {
+      r0 = (int)((int64_t)n * c / chunks);
+      r1 = (int)((int64_t)n * (c + 1) / chunks);
+    };
+    std::vector<std::thread> ws;
+    for (int t = 0; t < T; ++t)
+      ws.emplace_back([&, t] {
+        for (int c = 0; c < chunks; ++c) {
+          int r0, r1;
+          chunk_rows(c, r0, r1);
+          const size_t e0 = (size_t)r0 * n, m = (size_t)(r1 - r0) * n;
+          const size_t a = e0 + m * t / T, b = e0 + m * (t + 1) / T;
+          for (size_t e = a; e < b; ++e) {
+            if (e + kPrefetch < b) prefetch_bf(Avals[e + kPrefetch]);
+            if (!flat_from_bf(Avals[e], Af[e])) {
+              wide.store(true);
+              break;
+            }
+          }
+          done[c].fetch_add(1);
+          if (t == 0) {
+            while (done[c].load() < T) std::this_thread::yield();
+            if (!wide.load() && dev_st.load() == 0) {
+              std::string e2;
+              const int r = S.device_convert_rows(r0, r1, e2);
+              if (r) {
+                dev_err = e2;
+                dev_st.store(r);
+              }
+            }
+          }
+        }
+      });
+    for (auto &w : ws) w.join();
+    if (dev_st.load()) {
+      err = dev_err;
+      return dev_st.load();
+    }
+    ok = !wide.load();
+    plog.mark("A -> flat (host), chunked upload + convert");
+    int emax = INT_MIN;
+    double hs = 0.0;
+    if (ok) {
+      st = S.device_convert_end(&emax, &hs, err);
+      if (st != 0 && st != 5) return st;
+      ok = st == 0;
+      plog.mark("device convert");
+    }
+    if (ok) {
+      af_on_host = false;
+      head_emax.assign(T, INT_MIN);
+      head_sum.assign(T, 0.0);
+      head_emax[0] = emax;
+      head_sum[0] = hs;
+    } else {
+      dev_conv = false;  // a value wider than 640 bits or a head out of
+                         // range: the host pass below (bn fallback inside)
+    }
+  }
+  if (fast && !dev_conv) {
     // one pass: fixed-width value, its k binary64 heads (bf_to_multicomp),
     // the fixed-width copy (unless a second pass writes it) and, per
     // thread, the largest head exponent with the sum of the heads' squares
@@ -491,7 +590,7 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
         err = "value does not fit in binary64";
         return 5;
       }
-  } else {
+  } else if (!fast) {
     if ((st = to_planes(Avals, k, a_pl.p, nn, err, threads))) return st;
     std::vector<BF> sq(Avals.size());
     par_rows(Avals.size(), threads, [&](size_t a, size_t b) {
@@ -536,7 +635,8 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
       }
     }
   }
-  plog.mark(overlap ? "A -> planes" : "A -> fixed, planes");
+  plog.mark(dev_conv ? "A -> flat, GPU convert" :
+            overlap ? "A -> planes" : "A -> fixed, planes");
   if ((st = to_planes(Bvals, k, b_pl.data(), (size_t)n, err))) return st;
   std::vector<ff::F> Bf;
   bool use_dev = false;
@@ -547,7 +647,7 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
     begun = st == 0;
   }
   auto t1 = Clock::now();
-  if (overlap) {
+  if (overlap && !dev_conv) {
     // the fixed-width A, while the GPU factors (or before the synchronous
     // factorisation when the short side cannot overlap)
     par_rows(nn, threads, [&](size_t a, size_t b) {
@@ -950,4 +1050,108 @@ int refine_files(const char *a_path, const char *b_path, int short_k,
                      atol_s, max_iter, 0, S, out, err);
 }
 
+}  // namespace mpr
+
+namespace mpr {
+// The device long -> short conversion (convert.cu) against the host's
+// ff::from_bf + ff::to_multicomp: values of 1 .. 640 bits, exponents across
+// the binary64 range edges, runs of ones (rounding carries), exact halves.
+int64_t convert_selftest(int64_t iters, uint64_t seed, int p, int k,
+                         cudaStream_t s) {
+  if (iters <= 0 || p < 2 || p > 64 * ff::NL || k < 2 || k > 4) return -1;
+  uint64_t z = seed;
+  auto rnd = [&]() {
+    z += 0x9E3779B97F4A7C15ull;
+    uint64_t x = z;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+  };
+  std::vector<ff::F> flat(iters);
+  std::vector<ff::F> host_f(iters);
+  std::vector<double> host_c(4 * iters, 0.0);
+  std::vector<int> host_ok(iters);
+  for (int64_t it = 0; it < iters; ++it) {
+    BF v;
+    const int bits = 1 + (int)(rnd() % (64 * ff::NL));
+    bn::UBig m;
+    for (int b = 0; b < bits; b += 32) m.w.push_back((uint32_t)rnd());
+    m = m.shr((int64_t)m.w.size() * 32 - bits);
+    m.trim();
+    if (rnd() % 6 == 0) {  // runs of ones / exact halves
+      m = bn::UBig::sub(bn::UBig(1).shl(bits), bn::UBig(1 + rnd() % 2));
+      if (rnd() & 1) m = bn::UBig::add(m.shl(0), bn::UBig(1).shl(bits / 2));
+      m.trim();
+    }
+    if (m.zero() || rnd() % 50 == 0) {
+      v = BF();
+    } else {
+      v.sign = (rnd() & 1) ? 1 : -1;
+      v.man = m;
+      const int64_t kind = rnd() % 10;
+      const int64_t top = kind == 0 ? 1020 + (int64_t)(rnd() % 8)
+                          : kind == 1 ? -1015 - (int64_t)(rnd() % 12)
+                                      : (int64_t)(rnd() % 200) - 100;
+      v.exp = top - bits;
+    }
+    if (!flat_from_bf(v, flat[it])) {  // > 640 bits: the host path's
+      flat[it] = ff::F();               // (not compared)
+      flat[it].sign = 0;
+      std::memset(flat[it].m, 0, sizeof flat[it].m);
+      host_ok[it] = -1;
+      continue;
+    }
+    host_f[it] = ff::from_bf(v, p);
+    host_ok[it] = ff::to_multicomp(host_f[it], k, p, &host_c[4 * it]) ? 1 : 0;
+  }
+  void *dA = nullptr, *dh = nullptr, *dok = nullptr;
+  std::vector<ff::F> dev_f(iters);
+  std::vector<double> dev_c(4 * iters);
+  std::vector<int> dev_ok(iters);
+  int64_t bad = -1;
+  const size_t fb = sizeof(ff::F) * iters;
+  if (cudaMalloc(&dA, fb) == cudaSuccess &&
+      cudaMalloc(&dh, sizeof(double) * 4 * iters) == cudaSuccess &&
+      cudaMalloc(&dok, sizeof(int) * iters) == cudaSuccess &&
+      cudaMemcpy(dA, flat.data(), fb, cudaMemcpyHostToDevice) == cudaSuccess &&
+      mpk::long_to_short_selftest(k, p, dA, iters, static_cast<double *>(dh),
+                                  static_cast<int *>(dok), s) == cudaSuccess &&
+      cudaStreamSynchronize(s) == cudaSuccess &&
+      cudaMemcpy(dev_f.data(), dA, fb, cudaMemcpyDeviceToHost) == cudaSuccess &&
+      cudaMemcpy(dev_c.data(), dh, sizeof(double) * 4 * iters,
+                 cudaMemcpyDeviceToHost) == cudaSuccess &&
+      cudaMemcpy(dev_ok.data(), dok, sizeof(int) * iters,
+                 cudaMemcpyDeviceToHost) == cudaSuccess) {
+    bad = 0;
+    const int nl = (p + 63) >> 6;
+    for (int64_t it = 0; it < iters; ++it) {
+      if (host_ok[it] < 0) continue;
+      const ff::F &u = host_f[it], &w = dev_f[it];
+      bool same = u.sign == w.sign;
+      if (same && u.sign != 0) {
+        same = u.exp == w.exp;
+        for (int l = 0; l < ff::NL; ++l)
+          same = same && (l < nl ? u.m[l] == w.m[l] : w.m[l] == 0);
+      }
+      same = same && host_ok[it] == dev_ok[it];
+      if (same && host_ok[it])
+        same = std::memcmp(&host_c[4 * it], &dev_c[4 * it],
+                           sizeof(double) * k) == 0;
+      if (!same && bad < 3 && std::getenv("MPCORE_SELFTEST_VERBOSE")) {
+        std::fprintf(stderr,
+                     "convert mismatch %lld: host sign %d exp %lld ok %d "
+                     "c %a %a | dev sign %d exp %lld ok %d c %a %a | m0 %llx/%llx\n",
+                     (long long)it, u.sign, (long long)u.exp, host_ok[it],
+                     host_c[4 * it], host_c[4 * it + 1], w.sign,
+                     (long long)w.exp, dev_ok[it], dev_c[4 * it],
+                     dev_c[4 * it + 1], (unsigned long long)u.m[0],
+                     (unsigned long long)w.m[0]);
+      }
+      if (!same) ++bad;
+    }
+  }
+  for (void *q : {dA, dh, dok})
+    if (q) cudaFree(q);
+  return bad;
+}
 }  // namespace mpr

@@ -51,6 +51,28 @@ class ShortSolver {
                                  std::string &err) { return -1; }
   virtual int factor_solve_end(std::vector<double> &x_planes,
                                std::string &err) { return 6; }
+  // Optional: the long -> short conversion on the device (SURVEY §8(f)
+  // row 2).  `flat` (staging slot 0, n x n ff::F) holds A's exact values
+  // (un-normalised limbs); on return the device holds them rounded to p
+  // (for the device residual) and their k binary64 heads (the planes of
+  // the next factor_solve_begin, which then uploads only b), and *emax /
+  // *hsum are the heads' largest exponent (INT_MIN: all zero) and sum of
+  // squares scaled by 2^-2emax.  -> 0; 5 when a head leaves the binary64
+  // range (convert on the host instead); other: error
+  virtual bool device_convert_supported(int p) { return false; }
+  // in row chunks: begin, then rows [r0, r1) of `flat` once the host has
+  // written them (their upload and conversion overlap the host's next
+  // chunk), then end
+  virtual int device_convert_begin(int k, int n, int p, const void *flat,
+                                   std::string &err) { return 6; }
+  virtual int device_convert_rows(int r0, int r1, std::string &err) {
+    return 6;
+  }
+  virtual int device_convert_end(int *emax, double *hsum, std::string &err) {
+    return 6;
+  }
+  // the device's rounded long A into host memory (n x n ff::F)
+  virtual int download_long_A(void *dst, std::string &err) { return 6; }
   // Optional: the long residual b - A x on the device.
   // Values travel as fixed-width long floats (fastfloat.h ff::F, p <= 512).
   virtual bool residual_supported(int p) { return false; }
@@ -76,6 +98,11 @@ int refine_core(std::vector<bn::BF> &A, std::vector<bn::BF> &B, int n,
                 int short_k, int long_bits, const char *rtol, const char *atol,
                 int max_iter, int threads, ShortSolver &short_side, Report &out,
                 std::string &err);
+
+// the device conversion (convert.cu) against the host's ff::from_bf +
+// to_multicomp on iters random values at precision p, k heads: mismatches
+int64_t convert_selftest(int64_t iters, uint64_t seed, int p, int k,
+                         cudaStream_t s);
 
 // fastfloat.h against the generic big-integer path: mismatches over iters
 // random operand pairs at precision p (-1: p out of the fixed-width range)

@@ -46,7 +46,7 @@ def check(rep):
 
 
 @pytest.mark.parametrize("mode", ["bounds", "exact_fro", "split_factor",
-                                  "no_overlap"])
+                                  "no_overlap", "host_convert"])
 def test_config3_n1024_matches_reference(mode, monkeypatch):
     # bounds: the production path (asynchronous factorisation overlapping
     # the fixed-width conversion, products-off-the-chain residual)
@@ -56,6 +56,8 @@ def test_config3_n1024_matches_reference(mode, monkeypatch):
         monkeypatch.setenv("MPCORE_REFINE_SPLIT_FACTOR", "1")
     if mode == "no_overlap":
         monkeypatch.setenv("MPCORE_REFINE_NO_OVERLAP", "1")
+    if mode == "host_convert":   # (default: the conversion on the GPU)
+        monkeypatch.setenv("MPCORE_REFINE_HOST_CONVERT", "1")
     h = ctypes.c_uint64()
     assert nat.lib().mpcore_refine_config3(
         G["n"], G["seed"], G["kappa_exp10"], 3, 512, b"1e-100", b"0", 20, 0,

@@ -1,7 +1,8 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT"
-timeout 900 python -m pytest -q -x tests/test_gpu_config3.py tests/test_gpu_config3_fullsize.py tests/test_gpu_ffi.py tests/test_gpu_api.py tests/test_gpu_long_residual.py 2>&1 | tail -3
-for cfg in "MPCORE_RESIDUAL_VARIANT=2 MPCORE_REFINE_NO_OVERLAP=1" "MPCORE_RESIDUAL_VARIANT=2"; do
+timeout 900 python -m pytest -q -x tests/test_gpu_convert.py tests/test_gpu_config3.py tests/test_gpu_config3_fullsize.py tests/test_gpu_ffi.py tests/test_gpu_api.py tests/test_gpu_long_residual.py 2>&1 | tail -3
+for cfg in "MPCORE_REFINE_HOST_CONVERT=1" "MPCORE_X=1"; do
   env $cfg timeout 300 python bench.py --config 3 --steps 20 --warmup 3 --no-cpu > /tmp/c3.json 2>/dev/null
-  python -c "import json; d=json.load(open('/tmp/c3.json')); print('$cfg', round(d['value']*1e3,2), 'ms', {a: round(v*1e3,2) for a,v in d['timings_s'].items()})"
+  python -c "import json; d=json.load(open('/tmp/c3.json')); print('$cfg', round(d['value']*1e3,2), 'ms', {a: round(v*1e3,2) for a,v in d['timings_s'].items()}, d['result']['iterations'])"
 done
+MPCORE_REFINE_TIMERS=1 timeout 300 python bench.py --config 3 --steps 1 --warmup 1 --no-cpu 2>&1 >/dev/null | tail -12
