@@ -6,6 +6,8 @@
 // the reference's) residual bit for bit.  Each row is one sequential chain
 // of n dependent long multiply-adds: a thread per row, one warp per block
 // so the warps spread over the SMs.
+#include <cstdlib>
+
 #include "internal.h"
 #include "longfloat.cuh"
 #include "longwarp.cuh"
@@ -77,7 +79,9 @@ long_residual_warp_kernel(const lf::DF *__restrict__ A,
 // unchanged, so the result is the same bits; the chain is the adds only.
 constexpr int LR_PROD = 3, LR_RING = 8;
 
-__global__ void __launch_bounds__(32 * (1 + LR_PROD))
+template <int NP>  // producer warps
+
+__global__ void __launch_bounds__(32 * (1 + NP))
 long_residual_split_kernel(const lf::DF *__restrict__ A,
                            const lf::DF *__restrict__ x,
                            const lf::DF *__restrict__ b,
@@ -129,11 +133,11 @@ long_residual_split_kernel(const lf::DF *__restrict__ A,
       an = load(arow[j]);
       xn = load(x[j]);
     }
-    for (; j < n; j += LR_PROD) {
+    for (; j < n; j += NP) {
       const lw::WV aj = an, xj = xn;
-      if (j + LR_PROD < n) {
-        an = load(arow[j + LR_PROD]);
-        xn = load(x[j + LR_PROD]);
+      if (j + NP < n) {
+        an = load(arow[j + NP]);
+        xn = load(x[j + NP]);
       }
       const lw::WV pr = lw::mul(aj, xj, p);
       const int s = j % LR_RING;
@@ -252,9 +256,22 @@ cudaError_t long_residual(int p, int n, const void *A, const void *x,
     return cudaGetLastError();
   }
   if (variant == 2 && p <= 512) {
-    long_residual_split_kernel<<<n, 32 * (1 + LR_PROD), 0, s>>>(
-        static_cast<const lf::DF *>(A), static_cast<const lf::DF *>(x),
-        static_cast<const lf::DF *>(b), static_cast<lf::DF *>(res), n, p);
+    // producer warps per row (MPCORE_RESIDUAL_PRODUCERS, default 2)
+    static const int np = [] {
+      const char *e = std::getenv("MPCORE_RESIDUAL_PRODUCERS");
+      const int v = e ? std::atoi(e) : 2;
+      return v < 1 ? 1 : (v > 3 ? 3 : v);
+    }();
+    auto a2 = static_cast<const lf::DF *>(A);
+    auto x2 = static_cast<const lf::DF *>(x);
+    auto b2 = static_cast<const lf::DF *>(b);
+    auto r2 = static_cast<lf::DF *>(res);
+    if (np == 1)
+      long_residual_split_kernel<1><<<n, 64, 0, s>>>(a2, x2, b2, r2, n, p);
+    else if (np == 2)
+      long_residual_split_kernel<2><<<n, 96, 0, s>>>(a2, x2, b2, r2, n, p);
+    else
+      long_residual_split_kernel<3><<<n, 128, 0, s>>>(a2, x2, b2, r2, n, p);
     return cudaGetLastError();
   }
   if (variant == 0 && p <= 512) {
