@@ -439,14 +439,21 @@ cudaError_t ensure_rank(RankWork &r, int k, int n, int nb) {
   }
   if ((size_t)n <= r.nmax && (size_t)nb <= r.nbmax && k <= r.kmax)
     return cudaSuccess;
-  if ((e = cudaStreamSynchronize(r.S))) return e;
-  for (auto *p : {(void *)r.slot[0], (void *)r.slot[1], (void *)r.lists,
-                  (void *)r.swaps_all, (void *)r.status_all,
-                  (void *)r.tswaps, (void *)r.v, (void *)r.tmp})
-    if (p) cudaFree(p);
+  // grow-only: the new sizes cover every earlier request
   const size_t nn = std::max((size_t)n, r.nmax),
                bb = std::max((size_t)nb, r.nbmax);
   const int kk = std::max(k, r.kmax);
+  if ((e = cudaStreamSynchronize(r.S))) return e;
+  if ((e = cudaStreamSynchronize(r.C))) return e;
+  void **bufs[] = {(void **)&r.slot[0], (void **)&r.slot[1], (void **)&r.lists,
+                   (void **)&r.swaps_all, (void **)&r.status_all,
+                   (void **)&r.tswaps, (void **)&r.v, (void **)&r.tmp};
+  for (void **p : bufs) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;  // (a failed allocation below leaves no dangling pointer)
+  }
+  r.nmax = r.nbmax = 0;
+  r.kmax = 0;
   r.slot_bytes = HDR_BYTES + (size_t)kk * nn * bb * sizeof(double);
   const size_t nblk = nn + 2;  // per-panel status (nb >= 1)
   if ((e = cudaMalloc(&r.slot[0], r.slot_bytes)) ||
@@ -574,9 +581,16 @@ int dist_lu_solve(void *comm, int k, int n, int nb, int G,
   }
   std::vector<int> idx_of(G, -1);  // rank -> served index
   for (int i = 0; i < R; ++i) {
-    if ((e = ensure_rank(*DW.ranks[i], k, n, nb))) return fail(e, "workspace");
+    if (views[i].rank < 0 || views[i].rank >= G || idx_of[views[i].rank] >= 0) {
+      err = "ranks must be distinct and below the world size";
+      return 2;
+    }
     idx_of[views[i].rank] = i;
   }
+  if (phase_ms)
+    for (int i = 0; i < DIST_NPHASES; ++i) phase_ms[i] = 0.0;
+  for (int i = 0; i < R; ++i)
+    if ((e = ensure_rank(*DW.ranks[i], k, n, nb))) return fail(e, "workspace");
   Phases ph;
   ph.on = phase_ms != nullptr && R == 1;
   int64_t nlaunch = 0;
