@@ -511,7 +511,7 @@ def run_ours(args):
             "update_share_of_step": upd_ms / ms if ms else None,
             "traffic": traffic_bytes(k, n),
             "traffic_note": "DRAM bytes of one captured update launch "
-                            "(profiles/r01_traffic.json; its algorithmic "
+                            "(profiles/r02_traffic.json; its algorithmic "
                             "bytes are listed there)",
             "whole_step_frac": overall_rate / peak if peak else None,
             # flop-weighted (DFMA = 2 flops) against the DFMA issue peak
@@ -546,7 +546,7 @@ def traffic_bytes(k, n):
     launch (ncu --set full), when the capture matches this workload."""
     try:
         d = json.load(open(os.path.join(os.path.dirname(os.path.abspath(
-            __file__)), "profiles", "r01_traffic.json")))
+            __file__)), "profiles", "r02_traffic.json")))
     except (OSError, ValueError):
         return None
     return d["dram_bytes"] if (d.get("k"), d.get("n")) == (k, n) else None
