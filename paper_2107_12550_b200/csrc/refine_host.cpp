@@ -13,6 +13,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <climits>
 #include <cstddef>
 #include <chrono>
@@ -365,6 +368,69 @@ static bool flat_from_bf(const BF &v, ff::F &f) {
   return true;
 }
 
+// Worker threads kept for one refinement: the per-iteration loops over n
+// values (tens of microseconds of work) cannot pay a thread start-up each.
+// Workers spin briefly on a generation counter, then sleep on a condition
+// variable; run() splits [0, n) into contiguous chunks, the caller takes
+// the first.
+class SpinPool {
+ public:
+  explicit SpinPool(int threads) : T_(std::max(1, threads)) {
+    for (int t = 1; t < T_; ++t) ts_.emplace_back([this, t] { loop(t); });
+  }
+  ~SpinPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_.store(true);
+      gen_.fetch_add(1);
+    }
+    cv_.notify_all();
+    for (auto &t : ts_) t.join();
+  }
+  template <class F> void run(size_t n, F f) {
+    if (T_ == 1 || n < 64) {
+      f((size_t)0, n);
+      return;
+    }
+    job_ = [&](int t) { f(n * t / T_, n * (t + 1) / T_); };
+    done_.store(0);
+    {
+      std::lock_guard<std::mutex> g(m_);
+      gen_.fetch_add(1);
+    }
+    cv_.notify_all();
+    job_(0);
+    while (done_.load() < T_ - 1) {
+    }
+  }
+
+ private:
+  void loop(int t) {
+    uint64_t seen = 0;
+    for (;;) {
+      int spins = 0;
+      while (gen_.load() == seen && ++spins < 200000) {
+      }
+      if (gen_.load() == seen) {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_.load() != seen; });
+      }
+      seen = gen_.load();
+      if (stop_.load()) return;
+      job_(t);
+      done_.fetch_add(1);
+    }
+  }
+  int T_;
+  std::vector<std::thread> ts_;
+  std::function<void(int)> job_;
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<int> done_{0};
+  std::atomic<bool> stop_{false};
+  std::mutex m_;
+  std::condition_variable cv_;
+};
+
 // software prefetch of a value's heap-allocated mantissa limbs
 constexpr size_t kPrefetch = 24;
 static inline void prefetch_bf(const BF &v) {
@@ -700,28 +766,32 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
   // exactly whenever they span fewer than p_in - 56 bits (always, for the
   // renormalised values the GPU returns); otherwise the generic path
   const int pin = (int)p_in;
+  SpinPool pool(std::min(T, std::max(1, n / 64)));
   auto lift_f = [&](const std::vector<double> &pl, std::vector<ff::F> &x) {
     x.resize(n);
-    for (int i = 0; i < n; ++i) {
-      double c[4];
-      int emax = INT_MIN, emin = INT_MAX;
-      for (int q = 0; q < k; ++q) {
-        c[q] = pl[(size_t)q * n + i];
-        if (c[q] != 0.0) {
-          const int e = std::ilogb(c[q]);
-          emax = std::max(emax, e);
-          emin = std::min(emin, e);
+    pool.run((size_t)n, [&](size_t i0, size_t i1) {
+      for (size_t i = i0; i < i1; ++i) {
+        double c[4];
+        int emax = INT_MIN, emin = INT_MAX;
+        for (int q = 0; q < k; ++q) {
+          c[q] = pl[(size_t)q * n + i];
+          if (c[q] != 0.0) {
+            const int e = std::ilogb(c[q]);
+            emax = std::max(emax, e);
+            emin = std::min(emin, e);
+          }
         }
+        if (emax != INT_MIN && emax - emin > pin - 56) {
+          x[i] = ff::from_bf(lf_round(from_components(c, k, p_in), p), pi);
+          continue;
+        }
+        ff::F acc;
+        for (int q = 0; q < k; ++q)
+          if (c[q] != 0.0)
+            acc = ff::fadd(acc, ff::from_double(c[q], pin), pin);
+        x[i] = ff::round(acc, pin, pi);
       }
-      if (emax != INT_MIN && emax - emin > pin - 56) {
-        x[i] = ff::from_bf(lf_round(from_components(c, k, p_in), p), pi);
-        continue;
-      }
-      ff::F acc;
-      for (int q = 0; q < k; ++q)
-        if (c[q] != 0.0) acc = ff::fadd(acc, ff::from_double(c[q], pin), pin);
-      x[i] = ff::round(acc, pin, pi);
-    }
+    });
   };
   std::vector<BF> x;
   std::vector<ff::F> xf, resf, zf;
@@ -734,9 +804,15 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
   const BF one = from_int(1, p);
   const BF sqrt_n = lf_sqrt(from_int(n, p), p);
   std::vector<BF> res(n), work(n), z;
+  // (the squares in parallel, their sum in the reference's order)
+  std::vector<ff::F> sqv;
   auto norm2_f = [&](const std::vector<ff::F> &v) {
+    sqv.resize(v.size());
+    pool.run(v.size(), [&](size_t i0, size_t i1) {
+      for (size_t i = i0; i < i1; ++i) sqv[i] = ff::fmul(v[i], v[i], pi);
+    });
     ff::F acc;
-    for (const ff::F &s : v) acc = ff::fadd(acc, ff::fmul(s, s, pi), pi);
+    for (const ff::F &q : sqv) acc = ff::fadd(acc, q, pi);
     return lf_sqrt(ff::to_bf(acc), p);
   };
   std::string reason = "max_iter";
@@ -820,15 +896,22 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
     std::vector<double> w_pl((size_t)k * n);
     if (fast) {
       const ff::F cf = ff::from_bf(coef, pi);
-      for (int i = 0; i < n; ++i) {
-        const ff::F w = ff::fmul(resf[i], cf, pi);
-        double c[4];
-        if (!ff::to_multicomp(w, k, pi, c) &&
-            bn::to_multicomp(ff::to_bf(w), k, c)) {
-          err = "value does not fit in binary64";
-          return 5;
+      std::atomic<bool> overflow{false};
+      pool.run((size_t)n, [&](size_t i0, size_t i1) {
+        for (size_t i = i0; i < i1; ++i) {
+          const ff::F w = ff::fmul(resf[i], cf, pi);
+          double c[4];
+          if (!ff::to_multicomp(w, k, pi, c) &&
+              bn::to_multicomp(ff::to_bf(w), k, c)) {
+            overflow.store(true);
+            return;
+          }
+          for (int q = 0; q < k; ++q) w_pl[(size_t)q * n + i] = c[q];
         }
-        for (int q = 0; q < k; ++q) w_pl[(size_t)q * n + i] = c[q];
+      });
+      if (overflow.load()) {
+        err = "value does not fit in binary64";
+        return 5;
       }
     } else {
       for (int i = 0; i < n; ++i) work[i] = lf_mul(res[i], coef, p);
@@ -838,8 +921,10 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
     if (fast) {
       lift_f(x_pl, zf);
       const ff::F rn = ff::from_bf(res_norm, pi);
-      for (int i = 0; i < n; ++i)
-        xf[i] = ff::fadd(xf[i], ff::fmul(zf[i], rn, pi), pi);
+      pool.run((size_t)n, [&](size_t i0, size_t i1) {
+        for (size_t i = i0; i < i1; ++i)
+          xf[i] = ff::fadd(xf[i], ff::fmul(zf[i], rn, pi), pi);
+      });
     } else {
       lift(x_pl, z);
       for (int i = 0; i < n; ++i) x[i] = lf_add(x[i], lf_mul(z[i], res_norm, p), p);
