@@ -14,8 +14,9 @@ the same recipe, b = A*x_true in TD on the device).  A step = restore A
 
 Multi-GPU (torchrun, one rank per GPU): without --config, BASELINE config 4
 -- ONE DD n = 32768 system, column-block-cyclic over the ranks through the
-native distributed driver (strong scaling; `--config 4` at N = 1 is the
-same code with a one-rank world, the curve's first point).  Configs 1-3
+native distributed driver (strong scaling; under torchrun at N = 1, or with
+`--config 4`, the same code with a one-rank world is the curve's first
+point).  Configs 1-3
 are single-GPU workloads ("replicas only" under torchrun).  Barrier + max
 over ranks of the device time.
 """
@@ -1003,7 +1004,11 @@ def main():
                     help="config 4: write the per-panel phase timeline here")
     args = ap.parse_args()
     if args.config is None:
-        multi = int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.gpus > 1
+        # the multi-GPU launch (torchrun, any world size, or --gpus > 1)
+        # measures the north star's strong-scaling curve: config 4; a plain
+        # single-process run measures config 2 (the BASELINE metric's)
+        multi = (int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.gpus > 1
+                 or "TORCHELASTIC_RUN_ID" in os.environ)
         args.config = 4 if multi else 2
     if args.config == 4:
         args.k = args.k or 2
