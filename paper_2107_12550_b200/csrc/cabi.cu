@@ -719,12 +719,14 @@ IrWorkspace &ir_ws() {
   return w;
 }
 
-// production variant of the long residual (residual.cu): 2 = products off
-// the chain (default), 0 = warp per row; MPCORE_RESIDUAL_VARIANT overrides
+// production variant of the long residual (residual.cu): 5 = products in
+// their own kernel, then the chains (default); 2 = products on producer
+// warps beside the chain; 0 = warp per row; MPCORE_RESIDUAL_VARIANT
+// overrides
 int residual_variant() {
   static const int v = [] {
     const char *e = std::getenv("MPCORE_RESIDUAL_VARIANT");
-    return e ? std::atoi(e) : 2;
+    return e ? std::atoi(e) : 5;
   }();
   return v;
 }
@@ -1882,7 +1884,8 @@ int32_t mpcore_debug_panel_trace(uint64_t *out_ns, int64_t cap) {
 int32_t mpcore_debug_long_residual_selftest(int32_t n, int32_t prec,
                                             uint64_t seed, int32_t variant,
                                             int64_t *mismatches) {
-  if (!mismatches || variant < 0 || variant > 3) return MPCORE_BAD_DIMENSION;
+  if (!mismatches || variant < 0 || variant > 5 || variant == 3 || variant == 4)
+    return MPCORE_BAD_DIMENSION;
   DevLock L;
   if (L.st) return L.st;
   *mismatches = mpr::long_residual_selftest(n, prec, seed, device().stream,

@@ -57,8 +57,11 @@ struct LuWork {
 int num_sms();
 // IR residual b - A x at long precision p <= 512 on the device (residual.cu):
 // A row-major n x n, x, b, res length n, all as fixed-width long floats
-// (longfloat.cuh lf::DF = the host's ff::F); variant 0: a warp per row
-// (longwarp.cuh, the production path), 1: a thread per row (longfloat.cuh)
+// (longfloat.cuh lf::DF = the host's ff::F); variant 5 (production): the
+// n^2 products in one kernel (two per warp, longseg.cuh), then a warp per
+// row for the chain of adds; 2: the products on producer warps beside each
+// row's chain; 0: a warp per row doing both (longwarp.cuh); 1: a thread
+// per row (longfloat.cuh)
 cudaError_t long_residual(int p, int n, const void *A, const void *x,
                           const void *b, void *res, cudaStream_t s,
                           int variant = 0);

@@ -11,6 +11,7 @@
 #include "internal.h"
 #include "longfloat.cuh"
 #include "longwarp.cuh"
+#include "longseg.cuh"
 
 namespace mpk {
 
@@ -77,7 +78,7 @@ long_residual_warp_kernel(const lf::DF *__restrict__ A,
 // (the same warp-cooperative mul) ahead of it into a shared-memory ring,
 // published by a per-slot sequence flag.  Every operation and its order are
 // unchanged, so the result is the same bits; the chain is the adds only.
-constexpr int LR_PROD = 3, LR_RING = 8;
+constexpr int LR_RING = 8;
 
 template <int NP>  // producer warps
 
@@ -156,79 +157,72 @@ long_residual_split_kernel(const lf::DF *__restrict__ A,
   }
 }
 
-// Variant 3: as variant 2, but the chain of adds runs in one thread with
-// the limbs in registers (longfloat.cuh lf::add<N>: select-based shifters,
-// no cross-lane steps), the products still formed by the warp-cooperative
-// multiply; the ring carries them as lf::DF.
-template <int N>
-__global__ void __launch_bounds__(32 * (1 + LR_PROD))
-long_residual_split1_kernel(const lf::DF *__restrict__ A,
-                            const lf::DF *__restrict__ x,
-                            const lf::DF *__restrict__ b,
-                            lf::DF *__restrict__ res, int n, int p) {
-  __shared__ uint64_t ring_m[LR_RING][N];
-  __shared__ int64_t ring_e[LR_RING];
-  __shared__ int ring_s[LR_RING];
-  __shared__ volatile int ready[LR_RING];
-  __shared__ volatile int consumed;
-  const int row = blockIdx.x, warp = threadIdx.x >> 5, t = threadIdx.x & 31;
-  if (threadIdx.x < LR_RING) ready[threadIdx.x] = 0;
-  if (threadIdx.x == 0) consumed = 0;
-  __syncthreads();
-  const lf::DF *arow = A + (int64_t)row * n;
-  if (warp == 0) {
-    if (t != 0) return;
-    lf::DF acc = lf::zero();
-    for (int j = 0; j < n; ++j) {
-      const int s = j % LR_RING;
-      while (ready[s] != j + 1) {
-      }
-      __threadfence_block();
-      lf::DF pr = lf::zero();
-      pr.sign = ring_s[s];
-      pr.exp = ring_e[s];
-#pragma unroll
-      for (int i = 0; i < N; ++i) pr.m[i] = ring_m[s][i];
-      __threadfence_block();
-      consumed = j + 1;
-      acc = lf::add<N>(acc, pr, p);
-    }
-    res[row] = lf::add<N>(b[row], lf::neg(acc), p);
-    if (res[row].sign == 0) res[row].exp = 0;
-  } else {
-    auto load = [&](const lf::DF &v) {
-      lw::WV w;
-      w.m = t < lf::NL ? v.m[t] : 0ull;
-      w.exp = v.exp;
-      w.sign = v.sign;
-      return w;
-    };
-    const int pw = warp - 1;
-    int j = pw;
-    lw::WV an, xn;
-    if (j < n) {
-      an = load(arow[j]);
-      xn = load(x[j]);
-    }
-    for (; j < n; j += LR_PROD) {
-      const lw::WV aj = an, xj = xn;
-      if (j + LR_PROD < n) {
-        an = load(arow[j + LR_PROD]);
-        xn = load(x[j + LR_PROD]);
-      }
-      const lw::WV pr = lw::mul(aj, xj, p);
-      const int s = j % LR_RING;
-      while (lw::uni(consumed <= j - LR_RING)) __nanosleep(64);
-      __threadfence_block();
-      if (t < N) ring_m[s][t] = pr.m;
+// Variant 5 (production): the products and the chains in two kernels.
+// Every product mul(A_ij, x_j) is independent, so a first kernel forms all
+// n^2 of them -- two per warp, one per 16-lane segment (longseg.cuh: the
+// 2p-bit product needs 16 limbs, so a full warp left half its lanes idle) --
+// into a scratch matrix at full occupancy; then one warp per row runs only
+// its chain of correctly rounded adds over its row of products, the next
+// product's load in flight -- no producer/consumer hand-off inside the
+// chain.  (Fused into one cooperative launch, with the chains trailing the
+// production column block by column block, it was slower: the chains then
+// compete with the producers for issue slots.)
+// two products per warp (one per 16-lane segment, longseg.cuh)
+__global__ void __launch_bounds__(256)
+long_products2_kernel(const lf::DF *__restrict__ A,
+                      const lf::DF *__restrict__ x, lf::DF *__restrict__ P,
+                      int n, int p) {
+  const int t = threadIdx.x & 15, sg = (threadIdx.x >> 4) & 1;
+  const int64_t nn = (int64_t)n * n;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t e0 = 2 * wid; e0 < nn; e0 += 2 * nw) {
+    const int64_t e = e0 + sg;
+    if (e < nn) {  // (segment-uniform)
+      const lf::DF &a = A[e], &xv = x[e % n];
+      ls::WV wa, wx;
+      wa.m = t < lf::NL ? a.m[t] : 0ull;
+      wa.exp = a.exp;
+      wa.sign = a.sign;
+      wx.m = t < lf::NL ? xv.m[t] : 0ull;
+      wx.exp = xv.exp;
+      wx.sign = xv.sign;
+      const ls::WV pr = ls::mul(wa, wx, p);
+      if (t < lf::NL) P[e].m[t] = pr.m;
       if (t == 0) {
-        ring_e[s] = pr.exp;
-        ring_s[s] = pr.sign;
+        P[e].sign = pr.sign;
+        P[e].exp = pr.exp;
       }
-      __threadfence_block();
-      __syncwarp();
-      if (t == 0) ready[s] = j + 1;
     }
+  }
+}
+
+__global__ void __launch_bounds__(128)
+long_chain_kernel(const lf::DF *__restrict__ P, const lf::DF *__restrict__ b,
+                  lf::DF *__restrict__ res, int n, int p) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (lw::uni(row >= n)) return;
+  const int t = threadIdx.x & 31;
+  auto load = [&](const lf::DF &v) {
+    lw::WV w;
+    w.m = t < lf::NL ? v.m[t] : 0ull;
+    w.exp = v.exp;
+    w.sign = v.sign;
+    return w;
+  };
+  const lf::DF *prow = P + (int64_t)row * n;
+  lw::WV acc = lw::zero();
+  lw::WV nx = load(prow[0]);
+  for (int j = 0; j < n; ++j) {
+    const lw::WV pj = nx;
+    if (j + 1 < n) nx = load(prow[j + 1]);
+    acc = lw::add(acc, pj, p);
+  }
+  const lw::WV r = lw::add(load(b[row]), lw::neg(acc), p);
+  if (t < lf::NL) res[row].m[t] = r.m;
+  if (t == 0) {
+    res[row].sign = r.sign;
+    res[row].exp = r.sign == 0 ? 0 : r.exp;
   }
 }
 
@@ -238,21 +232,27 @@ cudaError_t long_residual(int p, int n, const void *A, const void *x,
                           const void *b, void *res, cudaStream_t s,
                           int variant) {
   if (n <= 0) return cudaSuccess;
-  if (variant == 3 && p <= 512) {
-    auto a3 = static_cast<const lf::DF *>(A);
-    auto x3 = static_cast<const lf::DF *>(x);
-    auto b3 = static_cast<const lf::DF *>(b);
-    auto r3 = static_cast<lf::DF *>(res);
-    switch ((p + 63) >> 6) {
-#define LR3_CASE(NN)                                                        \
-  case NN:                                                                  \
-    long_residual_split1_kernel<NN><<<n, 32 * (1 + LR_PROD), 0, s>>>(      \
-        a3, x3, b3, r3, n, p);                                              \
-    break;
-      LR3_CASE(1) LR3_CASE(2) LR3_CASE(3) LR3_CASE(4)
-      LR3_CASE(5) LR3_CASE(6) LR3_CASE(7) LR3_CASE(8)
-#undef LR3_CASE
+  if (variant == 5 && p <= 512) {
+    // scratch for the n^2 products (grow-only, kept)
+    static void *scratch = nullptr;
+    static size_t cap = 0;
+    const size_t need = (size_t)n * n * sizeof(lf::DF);
+    if (cap < need) {
+      if (scratch) cudaFree(scratch);
+      scratch = nullptr;
+      cap = 0;
+      cudaError_t e = cudaMalloc(&scratch, need);
+      if (e != cudaSuccess) return e;
+      cap = need;
     }
+    auto *P = static_cast<lf::DF *>(scratch);
+    long_products2_kernel<<<148 * 8, 256, 0, s>>>(
+        static_cast<const lf::DF *>(A), static_cast<const lf::DF *>(x), P, n,
+        p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    long_chain_kernel<<<(n + 3) / 4, 128, 0, s>>>(
+        P, static_cast<const lf::DF *>(b), static_cast<lf::DF *>(res), n, p);
     return cudaGetLastError();
   }
   if (variant == 2 && p <= 512) {

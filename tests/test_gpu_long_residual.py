@@ -11,11 +11,12 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 5])
 @pytest.mark.parametrize("prec", [53, 64, 65, 106, 200, 300, 424, 511, 512])
 @pytest.mark.parametrize("n", [1, 7, 33])
 def test_device_residual_matches_host(prec, n, variant):
-    # variant 2: products off the chain (production), 0: warp per row,
+    # variant 5: products kernel + chain kernel (production), 2: products
+    # on producer warps beside the chain, 0: warp per row,
     # 1: thread per row
     from paper_2107_12550_b200 import _native as nat
     m = ctypes.c_int64(-1)
@@ -25,7 +26,7 @@ def test_device_residual_matches_host(prec, n, variant):
     assert m.value == 0
 
 
-@pytest.mark.parametrize("variant", [0, 2, 3])
+@pytest.mark.parametrize("variant", [0, 2, 5])
 def test_device_residual_larger(variant):
     from paper_2107_12550_b200 import _native as nat
     m = ctypes.c_int64(-1)
