@@ -948,11 +948,21 @@ def run_config3(args):
                    "residuals": r["residuals"],
                    "max_abs_err_vs_ones": r["max_abs_err_vs_ones"]},
         "timings_s": tm,
+        # (bytes: the exact long A (96 B per element, flat), b as TD
+        # planes and as a long vector, x (long) for every residual and the
+        # TD right-hand side of every correction solve in; the long
+        # residual of every iteration and the TD solution of every solve
+        # out)
         "e2e": {"value": sec, "unit": "s", "h2d_bytes_per_step":
-                (3 * n * n + 3 * n * (r["iterations"] + 1)) * 8,
-                "d2h_bytes_per_step": 3 * n * (r["iterations"] + 1) * 8,
+                96 * n * n + 3 * n * 8 + 96 * n
+                + len(r["residuals"]) * 96 * n
+                + r["iterations"] * 3 * n * 8,
+                "d2h_bytes_per_step": len(r["residuals"]) * 96 * n
+                + (r["iterations"] + 1) * 3 * n * 8,
                 "path": "C ABI mpcore_refine_config3: host long system -> "
-                        "TD planes -> GPU LU -> host residual loop with GPU "
+                        "flat exact values -> GPU (round to 512 bits, TD "
+                        "heads, LU + first solve) -> residual loop: GPU "
+                        "long residuals, host norms / checks, GPU "
                         "correction solves"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
