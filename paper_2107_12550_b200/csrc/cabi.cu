@@ -688,6 +688,8 @@ struct IrWorkspace {
   // (device) and their page-locked copies
   void *dconv = nullptr, *hconv = nullptr;
   size_t dconvcap = 0, hconvcap = 0;
+  void *rflat = nullptr;  // compact exact values (device)
+  size_t rflatcap = 0;
   cudaStream_t up = nullptr;
   cudaEvent_t up_done = nullptr;
 };
@@ -951,7 +953,7 @@ class GpuShortSolver : public mpr::ShortSolver {
     return p <= 512 && claim();
   }
   int device_convert_begin(int k, int n, int p, const void *flat,
-                           std::string &err) override {
+                           bool compact, std::string &err) override {
     if (!claim()) { err = "no conversion workspace"; return MPCORE_INTERNAL; }
     DevLock L;
     if (L.st) { err = g_err; return L.st; }
@@ -963,6 +965,8 @@ class GpuShortSolver : public mpr::ShortSolver {
     cudaError_t e = ensure_buffers((size_t)k * plane * sizeof(double),
                                    (size_t)k * n * 8, (size_t)n * 4);
     if (e == cudaSuccess) e = grow_dev(&w.rA, w.rAcap, nn * LF_BYTES);
+    if (e == cudaSuccess && compact)
+      e = grow_dev(&w.rflat, w.rflatcap, nn * sizeof(mpk::LongFlat9));
     if (e == cudaSuccess) e = grow_dev(&w.dconv, w.dconvcap, sc);
     if (e == cudaSuccess) e = grow_host(&w.hconv, w.hconvcap, sc);
     char *dc = static_cast<char *>(w.dconv);
@@ -976,6 +980,7 @@ class GpuShortSolver : public mpr::ShortSolver {
     ck_ = k;
     cn_ = n;
     cp_ = p;
+    compact_ = compact;
     return MPCORE_OK;
   }
   int device_convert_rows(int r0, int r1, std::string &err) override {
@@ -986,14 +991,18 @@ class GpuShortSolver : public mpr::ShortSolver {
     const int n = cn_;
     const size_t plane = (size_t)n * (n + 1);
     char *dc = static_cast<char *>(w.dconv);
-    const size_t off = (size_t)r0 * n * LF_BYTES;
-    cudaError_t e = cudaMemcpyAsync(static_cast<char *>(w.rA) + off,
+    const size_t rec = compact_ ? sizeof(mpk::LongFlat9) : LF_BYTES;
+    const size_t off = (size_t)r0 * n * rec;
+    void *dst = compact_ ? w.rflat : w.rA;
+    cudaError_t e = cudaMemcpyAsync(static_cast<char *>(dst) + off,
                                     static_cast<char *>(w.stage) + off,
-                                    (size_t)(r1 - r0) * n * LF_BYTES,
+                                    (size_t)(r1 - r0) * n * rec,
                                     cudaMemcpyHostToDevice, D.stream);
     if (e == cudaSuccess)
-      e = mpk::long_to_short_rows(ck_, n, cp_, w.rA, r0, r1, a_, n + 1,
-                                  (int64_t)plane, reinterpret_cast<int *>(dc),
+      e = mpk::long_to_short_rows(ck_, n, cp_, w.rA,
+                                  compact_ ? w.rflat : nullptr, r0, r1, a_,
+                                  n + 1, (int64_t)plane,
+                                  reinterpret_cast<int *>(dc),
                                   reinterpret_cast<int *>(dc + 4), D.stream);
     if (e != cudaSuccess) {
       err = cudaGetErrorString(e);
@@ -1207,6 +1216,7 @@ class GpuShortSolver : public mpr::ShortSolver {
   bool upload_pending_ = false;
   bool inflight_ = false;  // factor_solve_begin without its end yet
   int ck_ = 0, cn_ = 0, cp_ = 0;  // the conversion in flight
+  bool compact_ = false;
   bool a_on_device_ = false;   // device_convert filled a_'s A planes
   bool af_on_device_ = false;  // ... and the rounded long A (w.rA)
   bool tried_ = false;

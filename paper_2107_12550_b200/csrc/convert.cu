@@ -180,16 +180,25 @@ __device__ bool to_multicomp(const lf::DF &r0, int k, int p, double *out) {
 // A[e] (flat exact value) -> A[e] rounded to p; its k heads into the planes
 // (element (i, j) of plane c at pl[c * plane + i * ld + j]); the largest
 // head exponent into *emax; *bad when a head leaves the binary64 range
-template <int N>
+template <int N, bool COMPACT>
 __global__ void __launch_bounds__(256)
-convert_kernel(lf::DF *__restrict__ A, int64_t e0, int64_t e1, int n, int k,
-               int p, double *__restrict__ pl, int64_t ld, int64_t plane,
+convert_kernel(lf::DF *__restrict__ A, const LongFlat9 *__restrict__ in,
+               int64_t e0, int64_t e1, int n, int k, int p,
+               double *__restrict__ pl, int64_t ld, int64_t plane,
                int *__restrict__ bad, int *__restrict__ emax) {
   int my_emax = INT_MIN;
   for (int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e1;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const lf::DF raw = A[e];
-    const lf::DF v = round_to(raw.sign, raw.m, CL, raw.exp, p);
+    lf::DF v;
+    if constexpr (COMPACT) {
+      const LongFlat9 f = in[e];
+      uint64_t w[CL];
+      for (int i = 0; i < CL; ++i) w[i] = i < 9 ? f.m[i] : 0ull;
+      v = round_to((int)(f.es & 3) - 1, w, CL, f.es >> 2, p);
+    } else {
+      const lf::DF raw = A[e];
+      v = round_to(raw.sign, raw.m, CL, raw.exp, p);
+    }
     A[e] = v;
     double c[4] = {0.0, 0.0, 0.0, 0.0};
     if (!to_multicomp<N>(v, k, p, c)) atomicOr(bad, 1);
@@ -232,14 +241,24 @@ headsum_kernel(const double *__restrict__ pl, int64_t ld, int n,
   if (threadIdx.x == 0) partials[blockIdx.x] = red[0];
 }
 
-// selftest: the device round + peel of flat values, for the host to compare
+// selftest: the device round + peel of flat values (in place, or from the
+// compact records when in9 is set), for the host to compare
 template <int N>
-__global__ void convert_only_kernel(lf::DF *A, int64_t count, int k, int p,
+__global__ void convert_only_kernel(lf::DF *A, const LongFlat9 *in9,
+                                    int64_t count, int k, int p,
                                     double *heads, int *ok) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const lf::DF raw = A[e];
-    const lf::DF v = round_to(raw.sign, raw.m, CL, raw.exp, p);
+    lf::DF v;
+    if (in9) {
+      const LongFlat9 f = in9[e];
+      uint64_t w[CL];
+      for (int i = 0; i < CL; ++i) w[i] = i < 9 ? f.m[i] : 0ull;
+      v = round_to((int)(f.es & 3) - 1, w, CL, f.es >> 2, p);
+    } else {
+      const lf::DF raw = A[e];
+      v = round_to(raw.sign, raw.m, CL, raw.exp, p);
+    }
     A[e] = v;
     ok[e] = to_multicomp<N>(v, k, p, heads + 4 * e) ? 1 : 0;
   }
@@ -268,17 +287,24 @@ cudaError_t long_to_short_init(int *d_bad, int *d_emax, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t long_to_short_rows(int k, int n, int p, void *A, int r0, int r1,
-                               double *planes, int64_t ld, int64_t plane,
-                               int *d_bad, int *d_emax, cudaStream_t s) {
+cudaError_t long_to_short_rows(int k, int n, int p, void *A, const void *in,
+                               int r0, int r1, double *planes, int64_t ld,
+                               int64_t plane, int *d_bad, int *d_emax,
+                               cudaStream_t s) {
   const int64_t e0 = (int64_t)r0 * n, e1 = (int64_t)r1 * n;
   if (e1 <= e0) return cudaSuccess;
   const int grid = (int)std::min<int64_t>((e1 - e0 + 255) / 256, 148 * 16);
   auto *a = static_cast<lf::DF *>(A);
-  CONV_SWITCH((p + 63) >> 6,
-              (convert_kernel<N><<<grid, 256, 0, s>>>(a, e0, e1, n, k, p,
-                                                      planes, ld, plane, d_bad,
-                                                      d_emax)))
+  auto *f = static_cast<const LongFlat9 *>(in);
+  if (f) {
+    CONV_SWITCH((p + 63) >> 6,
+                (convert_kernel<N, true><<<grid, 256, 0, s>>>(
+                    a, f, e0, e1, n, k, p, planes, ld, plane, d_bad, d_emax)))
+  } else {
+    CONV_SWITCH((p + 63) >> 6,
+                (convert_kernel<N, false><<<grid, 256, 0, s>>>(
+                    a, f, e0, e1, n, k, p, planes, ld, plane, d_bad, d_emax)))
+  }
   return cudaGetLastError();
 }
 
@@ -292,12 +318,14 @@ cudaError_t long_to_short_stats(int n, const double *planes, int64_t ld,
 
 int long_to_short_partials() { return CONV_PARTIALS; }
 
-cudaError_t long_to_short_selftest(int k, int p, void *A, int64_t count,
-                                   double *heads, int *ok, cudaStream_t s) {
+cudaError_t long_to_short_selftest(int k, int p, void *A, const void *in9,
+                                   int64_t count, double *heads, int *ok,
+                                   cudaStream_t s) {
   auto *a = static_cast<lf::DF *>(A);
+  auto *f9 = static_cast<const LongFlat9 *>(in9);
   const int grid = (int)std::min<int64_t>((count + 255) / 256, 148 * 8);
   CONV_SWITCH((p + 63) >> 6,
-              (convert_only_kernel<N><<<grid, 256, 0, s>>>(a, count, k, p,
+              (convert_only_kernel<N><<<grid, 256, 0, s>>>(a, f9, count, k, p,
                                                            heads, ok)))
   return cudaGetLastError();
 }

@@ -71,16 +71,26 @@ cudaError_t long_residual(int p, int n, const void *A, const void *x,
 // binary64 range and the largest head exponent (*d_emax); then the
 // long_to_short_partials() per-block sums of the heads' squares scaled by
 // 2^-emax
+// A's exact values as uploaded when every mantissa fits 576 bits (80 B
+// instead of lf::DF's 96): es = exponent * 4 + sign + 1
+struct LongFlat9 {
+  int64_t es;
+  uint64_t m[9];
+};
 cudaError_t long_to_short_init(int *d_bad, int *d_emax, cudaStream_t s);
-cudaError_t long_to_short_rows(int k, int n, int p, void *A, int r0, int r1,
-                               double *planes, int64_t ld, int64_t plane,
-                               int *d_bad, int *d_emax, cudaStream_t s);
+// in == null: A holds the flat values (lf::DF) and is converted in place;
+// else in (LongFlat9, rows [r0, r1)) is converted into A
+cudaError_t long_to_short_rows(int k, int n, int p, void *A, const void *in,
+                               int r0, int r1, double *planes, int64_t ld,
+                               int64_t plane, int *d_bad, int *d_emax,
+                               cudaStream_t s);
 cudaError_t long_to_short_stats(int n, const double *planes, int64_t ld,
                                 const int *d_emax, double *d_partials,
                                 cudaStream_t s);
 int long_to_short_partials();
-cudaError_t long_to_short_selftest(int k, int p, void *A, int64_t count,
-                                   double *heads, int *ok, cudaStream_t s);
+cudaError_t long_to_short_selftest(int k, int p, void *A, const void *in9,
+                                   int64_t count, double *heads, int *ok,
+                                   cudaStream_t s);
 // diagnostics: per-panel kernel stamps into buf ([4 * n] u64) or off (null)
 cudaError_t lu_stamps_enable(unsigned long long *buf);
 

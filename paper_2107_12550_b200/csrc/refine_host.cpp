@@ -431,6 +431,18 @@ class SpinPool {
   std::condition_variable cv_;
 };
 
+// the compact record (mpk::LongFlat9: exponent and sign in one word, 9
+// limbs); false when the mantissa is wider than 576 bits
+static bool flat9_from_bf(const BF &v, mpk::LongFlat9 &f) {
+  const size_t n32 = v.man.w.size();
+  if (n32 > 18) return false;
+  f.es = (v.sign == 0 ? (int64_t)0 : v.exp) * 4 + (v.sign + 1);
+  std::memset(f.m, 0, sizeof f.m);
+  if (n32 && v.sign != 0)
+    std::memcpy(f.m, v.man.w.data(), n32 * sizeof(uint32_t));
+  return true;
+}
+
 // software prefetch of a value's heap-allocated mantissa limbs
 constexpr size_t kPrefetch = 24;
 static inline void prefetch_bf(const BF &v) {
@@ -539,58 +551,71 @@ int refine_core(std::vector<BF> &Avals, std::vector<BF> &Bvals, int n,
                   std::getenv("MPCORE_REFINE_HOST_CONVERT") == nullptr;
   if (dev_conv) {
     // row chunks: the host flattens chunk c + 1 while chunk c uploads and
-    // converts
-    std::atomic<bool> wide{false};
-    bool ok = true;
-    st = S.device_convert_begin(k, n, pi, Af.p, err);
-    if (st) return st;
-    const int chunks = std::max(1, std::min(8, n / 64));
-    // every thread flattens its share of each chunk in turn; thread 0 then
-    // waits for the chunk's other shares and hands it to the device, while
-    // the others already work on the next chunk
-    std::vector<std::atomic<int>> done(chunks);
-    for (auto &d : done) d.store(0);
-    std::atomic<int> dev_st{0};
-    std::string dev_err;
+    // converts.  First in the compact 80-byte records (every mantissa of at
+    // most 576 bits, the common case); a wider value restarts the pass in
+    // the full ff::F layout.
+    bool ok = false;
+    static const int chunk_env = [] {
+      const char *e = std::getenv("MPCORE_CONVERT_CHUNKS");
+      return e ? std::atoi(e) : 8;
+    }();
+    const int chunks = std::max(1, std::min(chunk_env, n / 64));
     auto chunk_rows = [&](int c, int &r0, int &r1) {
       r0 = (int)((int64_t)n * c / chunks);
       r1 = (int)((int64_t)n * (c + 1) / chunks);
     };
-    std::vector<std::thread> ws;
-    for (int t = 0; t < T; ++t)
-      ws.emplace_back([&, t] {
-        for (int c = 0; c < chunks; ++c) {
-          int r0, r1;
-          chunk_rows(c, r0, r1);
-          const size_t e0 = (size_t)r0 * n, m = (size_t)(r1 - r0) * n;
-          const size_t a = e0 + m * t / T, b = e0 + m * (t + 1) / T;
-          for (size_t e = a; e < b; ++e) {
-            if (e + kPrefetch < b) prefetch_bf(Avals[e + kPrefetch]);
-            if (!flat_from_bf(Avals[e], Af[e])) {
-              wide.store(true);
-              break;
+    auto *flat9 = reinterpret_cast<mpk::LongFlat9 *>(Af.p);
+    for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+      const bool compact = attempt == 0;
+      std::atomic<bool> wide{false};
+      st = S.device_convert_begin(k, n, pi, Af.p, compact, err);
+      if (st) return st;
+      // every thread flattens its share of each chunk in turn; thread 0
+      // then waits for the chunk's other shares and hands it to the
+      // device, while the others already work on the next chunk
+      std::vector<std::atomic<int>> done(chunks);
+      for (auto &d : done) d.store(0);
+      std::atomic<int> dev_st{0};
+      std::string dev_err;
+      std::vector<std::thread> ws;
+      for (int t = 0; t < T; ++t)
+        ws.emplace_back([&, t] {
+          for (int c = 0; c < chunks; ++c) {
+            int r0, r1;
+            chunk_rows(c, r0, r1);
+            const size_t e0 = (size_t)r0 * n, m = (size_t)(r1 - r0) * n;
+            const size_t a = e0 + m * t / T, b = e0 + m * (t + 1) / T;
+            for (size_t e = a; e < b && !wide.load(std::memory_order_relaxed);
+                 ++e) {
+              if (e + kPrefetch < b) prefetch_bf(Avals[e + kPrefetch]);
+              const bool fits = compact ? flat9_from_bf(Avals[e], flat9[e])
+                                        : flat_from_bf(Avals[e], Af[e]);
+              if (!fits) {
+                wide.store(true);
+                break;
+              }
             }
-          }
-          done[c].fetch_add(1);
-          if (t == 0) {
-            while (done[c].load() < T) std::this_thread::yield();
-            if (!wide.load() && dev_st.load() == 0) {
-              std::string e2;
-              const int r = S.device_convert_rows(r0, r1, e2);
-              if (r) {
-                dev_err = e2;
-                dev_st.store(r);
+            done[c].fetch_add(1);
+            if (t == 0) {
+              while (done[c].load() < T) std::this_thread::yield();
+              if (!wide.load() && dev_st.load() == 0) {
+                std::string e2;
+                const int r = S.device_convert_rows(r0, r1, e2);
+                if (r) {
+                  dev_err = e2;
+                  dev_st.store(r);
+                }
               }
             }
           }
-        }
-      });
-    for (auto &w : ws) w.join();
-    if (dev_st.load()) {
-      err = dev_err;
-      return dev_st.load();
+        });
+      for (auto &w : ws) w.join();
+      if (dev_st.load()) {
+        err = dev_err;
+        return dev_st.load();
+      }
+      ok = !wide.load();
     }
-    ok = !wide.load();
     plog.mark("A -> flat (host), chunked upload + convert");
     int emax = INT_MIN;
     double hs = 0.0;
@@ -1189,28 +1214,63 @@ int64_t convert_selftest(int64_t iters, uint64_t seed, int p, int k,
     host_f[it] = ff::from_bf(v, p);
     host_ok[it] = ff::to_multicomp(host_f[it], k, p, &host_c[4 * it]) ? 1 : 0;
   }
-  void *dA = nullptr, *dh = nullptr, *dok = nullptr;
+  // the compact records too (values of at most 576 bits)
+  std::vector<mpk::LongFlat9> flat9(iters);
+  std::vector<int> has9(iters, 0);
+  for (int64_t it = 0; it < iters; ++it) {
+    if (host_ok[it] < 0) continue;
+    BF v;
+    v.sign = flat[it].sign;
+    v.exp = flat[it].exp;
+    for (int l = 0; l < ff::NL; ++l) {
+      v.man.w.push_back((uint32_t)flat[it].m[l]);
+      v.man.w.push_back((uint32_t)(flat[it].m[l] >> 32));
+    }
+    v.man.trim();
+    has9[it] = flat9_from_bf(v, flat9[it]) ? 1 : 0;
+  }
+  void *dA = nullptr, *dh = nullptr, *dok = nullptr, *d9 = nullptr;
   std::vector<ff::F> dev_f(iters);
   std::vector<double> dev_c(4 * iters);
   std::vector<int> dev_ok(iters);
   int64_t bad = -1;
   const size_t fb = sizeof(ff::F) * iters;
-  if (cudaMalloc(&dA, fb) == cudaSuccess &&
-      cudaMalloc(&dh, sizeof(double) * 4 * iters) == cudaSuccess &&
-      cudaMalloc(&dok, sizeof(int) * iters) == cudaSuccess &&
-      cudaMemcpy(dA, flat.data(), fb, cudaMemcpyHostToDevice) == cudaSuccess &&
-      mpk::long_to_short_selftest(k, p, dA, iters, static_cast<double *>(dh),
-                                  static_cast<int *>(dok), s) == cudaSuccess &&
-      cudaStreamSynchronize(s) == cudaSuccess &&
-      cudaMemcpy(dev_f.data(), dA, fb, cudaMemcpyDeviceToHost) == cudaSuccess &&
-      cudaMemcpy(dev_c.data(), dh, sizeof(double) * 4 * iters,
-                 cudaMemcpyDeviceToHost) == cudaSuccess &&
-      cudaMemcpy(dev_ok.data(), dok, sizeof(int) * iters,
-                 cudaMemcpyDeviceToHost) == cudaSuccess) {
-    bad = 0;
+  // pass 0: the full records converted in place; pass 1: the compact ones
+  for (int pass = 0; pass < 2; ++pass) {
+    bool okc = true;
+    if (pass == 0)
+      okc = cudaMalloc(&dA, fb) == cudaSuccess &&
+            cudaMalloc(&dh, sizeof(double) * 4 * iters) == cudaSuccess &&
+            cudaMalloc(&dok, sizeof(int) * iters) == cudaSuccess &&
+            cudaMalloc(&d9, sizeof(mpk::LongFlat9) * iters) == cudaSuccess &&
+            cudaMemcpy(dA, flat.data(), fb, cudaMemcpyHostToDevice) ==
+                cudaSuccess &&
+            mpk::long_to_short_selftest(k, p, dA, nullptr, iters,
+                                        static_cast<double *>(dh),
+                                        static_cast<int *>(dok), s) ==
+                cudaSuccess;
+    else
+      okc = cudaMemcpy(d9, flat9.data(), sizeof(mpk::LongFlat9) * iters,
+                       cudaMemcpyHostToDevice) == cudaSuccess &&
+            mpk::long_to_short_selftest(k, p, dA, d9, iters,
+                                        static_cast<double *>(dh),
+                                        static_cast<int *>(dok), s) ==
+                cudaSuccess;
+    okc = okc && cudaStreamSynchronize(s) == cudaSuccess &&
+          cudaMemcpy(dev_f.data(), dA, fb, cudaMemcpyDeviceToHost) ==
+              cudaSuccess &&
+          cudaMemcpy(dev_c.data(), dh, sizeof(double) * 4 * iters,
+                     cudaMemcpyDeviceToHost) == cudaSuccess &&
+          cudaMemcpy(dev_ok.data(), dok, sizeof(int) * iters,
+                     cudaMemcpyDeviceToHost) == cudaSuccess;
+    if (!okc) {
+      bad = -1;
+      break;
+    }
+    if (pass == 0) bad = 0;
     const int nl = (p + 63) >> 6;
     for (int64_t it = 0; it < iters; ++it) {
-      if (host_ok[it] < 0) continue;
+      if (host_ok[it] < 0 || (pass == 1 && !has9[it])) continue;
       const ff::F &u = host_f[it], &w = dev_f[it];
       bool same = u.sign == w.sign;
       if (same && u.sign != 0) {
@@ -1222,20 +1282,13 @@ int64_t convert_selftest(int64_t iters, uint64_t seed, int p, int k,
       if (same && host_ok[it])
         same = std::memcmp(&host_c[4 * it], &dev_c[4 * it],
                            sizeof(double) * k) == 0;
-      if (!same && bad < 3 && std::getenv("MPCORE_SELFTEST_VERBOSE")) {
-        std::fprintf(stderr,
-                     "convert mismatch %lld: host sign %d exp %lld ok %d "
-                     "c %a %a | dev sign %d exp %lld ok %d c %a %a | m0 %llx/%llx\n",
-                     (long long)it, u.sign, (long long)u.exp, host_ok[it],
-                     host_c[4 * it], host_c[4 * it + 1], w.sign,
-                     (long long)w.exp, dev_ok[it], dev_c[4 * it],
-                     dev_c[4 * it + 1], (unsigned long long)u.m[0],
-                     (unsigned long long)w.m[0]);
-      }
+      if (!same && bad < 3 && std::getenv("MPCORE_SELFTEST_VERBOSE"))
+        std::fprintf(stderr, "convert mismatch (pass %d) at %lld\n", pass,
+                     (long long)it);
       if (!same) ++bad;
     }
   }
-  for (void *q : {dA, dh, dok})
+  for (void *q : {dA, dh, dok, d9})
     if (q) cudaFree(q);
   return bad;
 }

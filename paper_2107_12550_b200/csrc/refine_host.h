@@ -63,8 +63,12 @@ class ShortSolver {
   // in row chunks: begin, then rows [r0, r1) of `flat` once the host has
   // written them (their upload and conversion overlap the host's next
   // chunk), then end
+  // compact: `flat` holds mpk::LongFlat9 records (80 B, mantissas of at
+  // most 576 bits) instead of ff::F ones
   virtual int device_convert_begin(int k, int n, int p, const void *flat,
-                                   std::string &err) { return 6; }
+                                   bool compact, std::string &err) {
+    return 6;
+  }
   virtual int device_convert_rows(int r0, int r1, std::string &err) {
     return 6;
   }
