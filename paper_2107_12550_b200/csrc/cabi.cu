@@ -353,7 +353,12 @@ int make_pivot(const std::vector<int32_t> &swaps, uint64_t *out) {
 int default_nb(int k, int n) {
   (void)k;
   (void)n;
-  return 32;
+  // (experiments: MPCORE_LU_NB overrides the panel width)
+  static const int env = [] {
+    const char *e = std::getenv("MPCORE_LU_NB");
+    return e ? std::atoi(e) : 0;
+  }();
+  return env > 0 ? env : 32;
 }
 
 // factor obj in place; fills swaps; -> status (3 singular)
