@@ -283,60 +283,64 @@ __global__ void compose_lists_kernel(const int32_t *hdr, int J, int w,
 // v_i <- add(v_i, mul(U_ij, neg(x_j))) for j = J+w-1 down to J (the
 // reference's column sweep, linalg.py:512-519, operand order kept).  U is
 // the owner's local block (columns [0, w) of the view), x = v[J .. J+w).
-constexpr int BU_ROWS = 128, BU_COLS = 16;
+// A thread per row: its U values come in chunks of CH consecutive columns
+// (a cache line per plane), the next chunk's loads in flight while the
+// current chunk's madds run; the negated x in shared memory.
+constexpr int BU_ROWS = 128;
 template <int K>
 __global__ void __launch_bounds__(BU_ROWS)
 back_update_kernel(int J, int w, MatView U, double *__restrict__ v,
                    int64_t vplane) {
-  extern __shared__ double smb[];
-  double *xs = smb;                              // [w][K] negated x
-  double *tile = smb + (size_t)w * K;            // [K][BU_ROWS][BU_COLS + 1]
-  constexpr int TS = BU_COLS + 1;
+  constexpr int CH = K == 2 ? 16 : 8;
+  extern __shared__ double xs[];  // [w][K] negated x
   for (int e = threadIdx.x; e < w * K; e += BU_ROWS) {
     const int j = e / K, c = e % K;
     xs[e] = -v[c * vplane + J + j];
   }
-  const int i0 = blockIdx.x * BU_ROWS, i = i0 + threadIdx.x;
+  __syncthreads();
+  const int i = blockIdx.x * BU_ROWS + threadIdx.x;
+  if (i >= J) return;
   double acc[K];
 #pragma unroll
-  for (int c = 0; c < K; ++c) acc[c] = i < J ? v[c * vplane + i] : 0.0;
-  for (int c1 = w; c1 > 0; c1 -= BU_COLS) {
-    const int c0 = max(0, c1 - BU_COLS), nc = c1 - c0;
-    __syncthreads();
-    for (int e = threadIdx.x; e < BU_ROWS * BU_COLS; e += BU_ROWS) {
-      const int r = e / BU_COLS, cc = e % BU_COLS;
-      if (i0 + r < J && cc < nc) {
+  for (int c = 0; c < K; ++c) acc[c] = v[c * vplane + i];
+  const double *row = U.p + (int64_t)i * U.ld;
+  double cur[CH][K], nxt[CH][K];
+  // chunk t covers columns [c1 - CH, c1), c1 = w - t * CH, descending
+  auto fetch = [&](int c1, double (&dst)[CH][K]) {
 #pragma unroll
-        for (int c = 0; c < K; ++c)
-          tile[(c * BU_ROWS + r) * TS + cc] =
-              U.p[c * U.plane + (int64_t)(i0 + r) * U.ld + c0 + cc];
-      }
+    for (int q = 0; q < CH; ++q) {
+      const int col = c1 - CH + q;
+#pragma unroll
+      for (int c = 0; c < K; ++c)
+        dst[q][c] = col >= 0 ? row[c * U.plane + col] : 0.0;
     }
-    __syncthreads();
-    if (i < J) {
-      for (int cc = nc - 1; cc >= 0; --cc) {
-        double u[K], t[K], o[K];
+  };
+  fetch(w, cur);
+  for (int c1 = w; c1 > 0; c1 -= CH) {
+    if (c1 - CH > 0) fetch(c1 - CH, nxt);
 #pragma unroll
-        for (int c = 0; c < K; ++c)
-          u[c] = tile[(c * BU_ROWS + threadIdx.x) * TS + cc];
-        mc::mul<K>(u, xs + (size_t)(c0 + cc) * K, t);
-        mc::add<K>(acc, t, o);
+    for (int q = CH - 1; q >= 0; --q) {
+      const int col = c1 - CH + q;
+      if (col < 0) break;
+      double t[K], o[K];
+      mc::mul<K>(cur[q], xs + (size_t)col * K, t);
+      mc::add<K>(acc, t, o);
 #pragma unroll
-        for (int c = 0; c < K; ++c) acc[c] = o[c];
-      }
+      for (int c = 0; c < K; ++c) acc[c] = o[c];
     }
-  }
-  if (i < J) {
 #pragma unroll
-    for (int c = 0; c < K; ++c) v[c * vplane + i] = acc[c];
+    for (int q = 0; q < CH; ++q)
+#pragma unroll
+      for (int c = 0; c < K; ++c) cur[q][c] = nxt[q][c];
   }
+#pragma unroll
+  for (int c = 0; c < K; ++c) v[c * vplane + i] = acc[c];
 }
 
 template <int K>
 cudaError_t back_update_k(int J, int w, MatView U, double *v, int64_t vplane,
                           cudaStream_t s) {
-  const size_t smem = ((size_t)w * K + (size_t)K * BU_ROWS * (BU_COLS + 1)) *
-                      sizeof(double);
+  const size_t smem = (size_t)w * K * sizeof(double);
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(
