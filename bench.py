@@ -707,6 +707,9 @@ def run_dist(args):
             room = psutil.virtual_memory().available > 3 * M0.numel() * 8
         except Exception:
             room = False
+        # one decision for every rank (each one's host memory check runs
+        # while the others pin theirs): all run the e2e leg or none
+        room = max_over_ranks(pg, 0.0 if room else 1.0) == 0.0
         if room:
             hM = torch.empty(M0.shape, dtype=torch.float64, pin_memory=True)
             hM.copy_(M0.cpu())
