@@ -224,8 +224,9 @@ def set_planes(h, planes):
 
 # host arrays an asynchronous copy still reads or writes: kept alive here
 # until sync() returns (a dropped array would otherwise be freed under the
-# DMA)
-_inflight = []
+# DMA); keyed by id so a loop re-using the same staging buffers without
+# sync() does not grow it
+_inflight = {}
 
 
 def set_planes_async(h, planes):
@@ -238,7 +239,7 @@ def set_planes_async(h, planes):
         raise ValueError("set_planes_async needs a C-contiguous float64 array")
     check(lib().mpcore_set_planes_async(h, dptr(planes), planes.size),
           "set_planes_async")
-    _inflight.append(planes)
+    _inflight[id(planes)] = planes
 
 
 def get_planes_async(h, out):
@@ -249,7 +250,7 @@ def get_planes_async(h, out):
         raise ValueError("get_planes_async needs a C-contiguous float64 array")
     check(lib().mpcore_get_planes_async(h, dptr(out), out.size),
           "get_planes_async")
-    _inflight.append(out)
+    _inflight[id(out)] = out
 
 
 def get_planes(h, shape, out=None):
@@ -403,7 +404,7 @@ def sm_count():
 
 def sync():
     check(lib().mpcore_sync(), "sync")
-    del _inflight[:]
+    _inflight.clear()
 
 
 class StreamTimer:
