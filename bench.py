@@ -1015,7 +1015,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-trace", default="",
                     help="config 4: write the per-panel phase timeline here")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="default run: skip the other single-GPU configs "
+                         "measured after the headline (the 'extras' key)")
     args = ap.parse_args()
+    explicit = args.config is not None or args.k is not None or \
+        args.n is not None
     if args.config is None:
         # the multi-GPU launch (torchrun, any world size, or --gpus > 1)
         # measures the north star's strong-scaling curve: config 4; a plain
@@ -1043,8 +1048,68 @@ def main():
         run_config3(args)
     elif args.config == 1:
         run_config1(args)
-    else:
+    elif explicit or args.no_extras or args.gpus > 1 or \
+            int(os.environ.get("WORLD_SIZE", "1")) > 1:
         run_ours(args)
+    else:
+        line = captured(run_ours, args)
+        line["extras"] = run_extras(args)
+        print(json.dumps(line))
+
+
+def captured(fn, args):
+    """Run one bench leg in this process and return its JSON line."""
+    import contextlib
+    import io
+    buf = io.StringIO()
+    with contextlib.redirect_stdout(buf):
+        fn(args)
+    return json.loads(buf.getvalue().strip().splitlines()[-1])
+
+
+def run_extras(args):
+    """The default run's supplementary legs, AFTER the headline's timed
+    region (so they cannot disturb it): the other single-GPU BASELINE
+    workloads -- config 2 in QD, the DD LU + solve at n = 2048, the config-1
+    GEMMs in DD/TD/QD and config 3 -- each with its own warm-up, CUDA-event
+    timing on the library stream and clock sampling, summarised to its
+    value, per-step time, e2e and roofline fractions, so every config's
+    number comes out of the driver's own run.  --no-extras skips them."""
+    legs = [("config2_qd_lu_solve_n2048", run_ours,
+             dict(config=2, k=4, n=2048, steps=5, warmup=3)),
+            ("dd_lu_solve_n2048", run_ours,
+             dict(config=2, k=2, n=2048, steps=10, warmup=3)),
+            ("config1_dd_gemm_n2048", run_config1,
+             dict(config=1, k=2, n=2048, steps=5, warmup=2)),
+            ("config1_td_gemm_n2048", run_config1,
+             dict(config=1, k=3, n=2048, steps=3, warmup=2)),
+            ("config1_qd_gemm_n2048", run_config1,
+             dict(config=1, k=4, n=2048, steps=3, warmup=2)),
+            ("config3_td_mpmath_ir_n1024", run_config3,
+             dict(config=3, k=3, n=1024, steps=5, warmup=2))]
+    out = {}
+    for name, fn, kw in legs:
+        a = argparse.Namespace(**vars(args))
+        a.no_cpu = True
+        for key, v in kw.items():
+            setattr(a, key, v)
+        try:
+            d = captured(fn, a)
+        except Exception as e:  # a leg's failure must not void the headline
+            out[name] = {"error": "%s: %s" % (type(e).__name__, e)}
+            continue
+        rf = d.get("roofline") or {}
+        e2e = d.get("e2e") or {}
+        out[name] = {
+            "metric": d["metric"], "value": d["value"], "unit": d["unit"],
+            "ms_per_step": d["ms_per_step"], "steps": d["steps"],
+            "warmup": d["warmup"], "higher_is_better": d["higher_is_better"],
+            "e2e": e2e.get("value"),
+            "dominant_kernel_frac": rf.get("frac"),
+            "whole_step_frac": rf.get("whole_step_frac"),
+            "clocks": d.get("clocks"),
+            **({"result": d["result"]} if "result" in d else {})}
+    return out
 
 
 if __name__ == "__main__":
