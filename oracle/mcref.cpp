@@ -62,6 +62,11 @@ INL void split(double a, double &hi, double &lo) {
 // mcfloat.py:92-102 (Dekker)
 INL void two_prod(double a, double b, double &p, double &e) {
   p = a * b;
+#ifdef MCREF_FMA_TWO_PROD
+  // (libmcref_fma.so only: the FMA form the CUDA path uses)
+  e = std::fma(a, b, -p);
+  return;
+#endif
   double ahi, alo, bhi, blo;
   split(a, ahi, alo);
   split(b, bhi, blo);
