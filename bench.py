@@ -665,6 +665,14 @@ def run_dist(args):
     x = torch.zeros((k, n), dtype=torch.float64, device=M.device)
     with stdout_to_stderr():      # (NCCL's version banner goes to stdout)
         comm = NcclComm(world, rank)
+    try:
+        ncclv = ".".join(str(v) for v in torch.cuda.nccl.version())
+    except Exception:
+        ncclv = "?"
+    print("[bench config4] rank %d/%d: libmpcore NCCL communicator up on "
+          "cuda:%d (%s), NCCL %s, local columns %d of %d"
+          % (rank, world, local, torch.cuda.get_device_name(local), ncclv,
+             lc, n), file=sys.stderr, flush=True)
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
 
