@@ -11,7 +11,11 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("MPCORE_LIB") or os.path.join(_HERE, "libmpcore.so")  # (A/B builds)
+# MPCORE_EXACT_RANGE=1: the build whose two_prod reproduces the reference's
+# Dekker bits outside the binary64 band too (mc.cuh; 12-19 % slower)
+LIB_PATH = os.environ.get("MPCORE_LIB") or os.path.join(
+    _HERE, "libmpcore_exact.so" if os.environ.get("MPCORE_EXACT_RANGE", "0")
+    not in ("", "0") else "libmpcore.so")  # (MPCORE_LIB: A/B builds)
 
 OK, BAD_HANDLE, BAD_DIMENSION, SINGULAR, BAD_PARSE, OVERFLOW, INTERNAL = \
     range(7)

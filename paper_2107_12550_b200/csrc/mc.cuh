@@ -42,6 +42,64 @@ MCI void two_prod(double a, double b, double &p, double &e) {
   p = mul_(a, b);
   e = __fma_rn(a, b, -p);
 }
+// The reference's two_prod is Dekker's splitting form (mcfloat.py:79-102).
+// Its error term equals the FMA form's RN(a b - p) whenever the split cannot
+// overflow (|a|, |b| < 2**996) and no partial product underflows (a, b
+// normal, |p| >= 2**-959), and both are +0 when an operand is +-0 and the
+// other's split cannot overflow (tests/test_range_edges.py).
+// The default build relies on that band (every BASELINE input lies deep
+// inside it).  libmpcore_exact.so (MPCORE_EXACT_RANGE=1) is compiled with
+// MPCORE_EXACT_TWO_PROD: each multiplication routine forms its products the
+// FMA way, tests all its pairs on the integer pipe (exponent fields), and
+// only outside the band re-forms its error terms with tp_ref -- the
+// reference's own sequence (NaN error terms for huge operands, its tails
+// near underflow) -- so every result keeps the reference's bits everywhere,
+// for 12-19 % of the FP64-bound throughput.
+#ifdef MPCORE_EXACT_TWO_PROD
+MCI bool tp_ok(double a, double b, double p) {
+  const unsigned ma = (unsigned)__double2hiint(a) & 0x7ff00000u,
+                 mb = (unsigned)__double2hiint(b) & 0x7ff00000u,
+                 mp = (unsigned)__double2hiint(p) & 0x7ff00000u;
+  return (ma - 0x00100000u < (2018u << 20)) &
+         (mb - 0x00100000u < (2018u << 20)) &
+         (mp - (64u << 20) < (1983u << 20));
+}
+static __device__ __noinline__ double tp_ref(double a, double b, double p) {
+  const unsigned ha = (unsigned)__double2hiint(a),
+                 hb = (unsigned)__double2hiint(b);
+  const bool za = ((ha & 0x7fffffffu) | (unsigned)__double2loint(a)) == 0u;
+  const bool zb = ((hb & 0x7fffffffu) | (unsigned)__double2loint(b)) == 0u;
+  if ((za && (hb & 0x7ff00000u) < (2019u << 20)) ||
+      (zb && (ha & 0x7ff00000u) < (2019u << 20)) || tp_ok(a, b, p))
+    return __fma_rn(a, b, -p);
+  const double S = 134217729.0;  // _SPLIT = 2**27 + 1
+  double t = __dmul_rn(S, a);
+  const double ahi = __dsub_rn(t, __dsub_rn(t, a)), alo = __dsub_rn(a, ahi);
+  t = __dmul_rn(S, b);
+  const double bhi = __dsub_rn(t, __dsub_rn(t, b)), blo = __dsub_rn(b, bhi);
+  return __dadd_rn(__dadd_rn(__dadd_rn(__dsub_rn(__dmul_rn(ahi, bhi), p),
+                                       __dmul_rn(ahi, blo)),
+                             __dmul_rn(alo, bhi)),
+                   __dmul_rn(alo, blo));
+}
+#define MC_EXACT_1(A0, B0, P, Q)                                  \
+  if (__builtin_expect(!tp_ok(A0, B0, P), 0)) Q = tp_ref(A0, B0, P);
+#define MC_EXACT_6(a, b)                                                   \
+  if (__builtin_expect(!(tp_ok(a[0], b[0], p00) & tp_ok(a[0], b[1], p01) & \
+                         tp_ok(a[1], b[0], p10) & tp_ok(a[0], b[2], p02) & \
+                         tp_ok(a[1], b[1], p11) & tp_ok(a[2], b[0], p20)), \
+                       0)) {                                              \
+    q00 = tp_ref(a[0], b[0], p00);                                        \
+    q01 = tp_ref(a[0], b[1], p01);                                        \
+    q10 = tp_ref(a[1], b[0], p10);                                        \
+    q02 = tp_ref(a[0], b[2], p02);                                        \
+    q11 = tp_ref(a[1], b[1], p11);                                        \
+    q20 = tp_ref(a[2], b[0], p20);                                        \
+  }
+#else
+#define MC_EXACT_1(A0, B0, P, Q)
+#define MC_EXACT_6(a, b)
+#endif
 
 // _sweep: bottom-up two_sum chain; residuals overwrite t[0..M-2].
 template <int M> MCI double sweep(double (&t)[M]) {
@@ -105,6 +163,7 @@ MCI void add2(const double *a, const double *b, double *o) {
 MCI void mul2(const double *a, const double *b, double *o) {
   double p, e;
   two_prod(a[0], b[0], p, e);
+  MC_EXACT_1(a[0], b[0], p, e)
   e = add_(e, add_(mul_(a[0], b[1]), mul_(a[1], b[0])));
   quick_two_sum(p, e, o[0], o[1]);
 }
@@ -124,6 +183,7 @@ MCI void mul3(const double *a, const double *b, double *o) {
   two_prod(a[0], b[2], p02, q02);
   two_prod(a[1], b[1], p11, q11);
   two_prod(a[2], b[0], p20, q20);
+  MC_EXACT_6(a, b)
   double t3 = add_(add_(add_(q02, q11), q20),
                    add_(mul_(a[1], b[2]), mul_(a[2], b[1])));
   double t[10] = {p00, p01, p10, q00, p02, p11, p20, q01, q10, t3};
@@ -146,6 +206,7 @@ MCI void mul4(const double *a, const double *b, double *o) {
   two_prod(a[0], b[2], p02, q02);
   two_prod(a[1], b[1], p11, q11);
   two_prod(a[2], b[0], p20, q20);
+  MC_EXACT_6(a, b)
   double t3 = add_(add_(add_(q02, q11), q20),
                    add_(add_(mul_(a[0], b[3]), mul_(a[3], b[0])),
                         add_(mul_(a[1], b[2]), mul_(a[2], b[1]))));
@@ -176,6 +237,15 @@ template <int K> MCI void mul_scalar(const double *a, double x, double *o) {
   double t[2 * K];
 #pragma unroll
   for (int c = 0; c < K; ++c) two_prod(a[c], x, t[c], t[K + c]);
+#ifdef MPCORE_EXACT_TWO_PROD
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < K; ++c) ok &= tp_ok(a[c], x, t[c]);
+  if (__builtin_expect(!ok, 0)) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) t[K + c] = tp_ref(a[c], x, t[c]);
+  }
+#endif
   cascade_compress<2 * K, K>(t, o);
 }
 // RN(1/b) when b lies well inside the normal range (|exponent| <= 423), else

@@ -114,6 +114,9 @@ def test_gpu_range_edges(k):
     from paper_2107_12550_b200.linalg import (DeviceMatrix, DeviceVector,
                                               device_solve)
     g = golden("range_k%d.npz" % k)
+    if nat.LIB_PATH.endswith("libmpcore_exact.so"):
+        _exact_checks()    # this process runs the exact-range build
+        return
 
     def ew(op, x, y):
         hx, hy = DeviceVector.from_planes(x), DeviceVector.from_planes(y)
@@ -160,3 +163,63 @@ def test_gpu_range_edges(k):
     with oracle.fma_two_prod():
         assert same_nan_aware(dc.download(),
                               oracle.gemm(g["gemm_A"], g["gemm_B"]))
+
+
+def _exact_checks():
+    """Run in a process with MPCORE_EXACT_RANGE=1: the exact-range build
+    against the reference's goldens, every element."""
+    from paper_2107_12550_b200 import _native as nat
+    from paper_2107_12550_b200.linalg import (DeviceMatrix, DeviceVector,
+                                              device_solve)
+    assert nat.LIB_PATH.endswith("libmpcore_exact.so"), nat.LIB_PATH
+    for k in KS:
+        g = golden("range_k%d.npz" % k)
+
+        def ew(op, x, y):
+            hx, hy = DeviceVector.from_planes(x), DeviceVector.from_planes(y)
+            ho = DeviceVector(x.shape[0], x.shape[1])
+            nat.check(nat.lib().mpcore_elementwise(op, hx.handle, hy.handle,
+                                                   ho.handle), "elementwise")
+            return ho.download()
+
+        assert same_nan_aware(ew(0, g["kern_a"], g["kern_b"]), g["kern_add"])
+        assert same_nan_aware(ew(1, g["kern_a"], g["kern_b"]), g["kern_mul"])
+        assert same_nan_aware(ew(2, g["kern_div_a"], g["kern_div_b"]),
+                              g["kern_div"])
+        for tag in ("tiny", "huge"):
+            for nb in (0, 8):
+                dm = DeviceMatrix.from_planes(g["lu_%s_A" % tag])
+                piv = dm.lu_factor(nb)
+                assert np.asarray(piv.swaps(), dtype=np.int32).tobytes() == \
+                    g["lu_%s_swaps" % tag].tobytes()
+                assert same_nan_aware(dm.download(), g["lu_%s_lu" % tag])
+                rhs = g["lu_%s_b" % tag]
+                bv = DeviceVector.from_planes(rhs)
+                xv = DeviceVector(k, rhs.shape[1])
+                device_solve(dm, piv, bv, xv)
+                assert same_nan_aware(xv.download(), g["lu_%s_x" % tag])
+        da = DeviceMatrix.from_planes(g["gemm_A"])
+        db = DeviceMatrix.from_planes(g["gemm_B"])
+        dc = DeviceMatrix(k, g["gemm_A"].shape[1], g["gemm_B"].shape[2])
+        nat.check(nat.lib().mpcore_mat_mul(da.handle, db.handle, dc.handle),
+                  "mat_mul")
+        assert same_nan_aware(dc.download(), g["gemm_C"])
+    print("exact-range build: all range goldens bit-identical")
+
+
+@pytest.mark.gpu
+def test_gpu_exact_range_build_matches_reference_everywhere():
+    """MPCORE_EXACT_RANGE=1 loads libmpcore_exact.so, whose two_prod takes
+    the reference's Dekker sequence outside the band: then every golden --
+    huge operands' NaNs included -- is reproduced bit for bit."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, MPCORE_EXACT_RANGE="1")
+    code = ("import sys; sys.path[:0] = [%r, %r]; import test_range_edges "
+            "as t; t._exact_checks()" % (here, os.path.dirname(here)))
+    r = subprocess.run([sys.executable, "-c", code], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "bit-identical" in r.stdout
