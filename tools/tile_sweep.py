@@ -1,6 +1,6 @@
 """Issue efficiency of each GEMM tile candidate at a many-wave update shape
 (C += (-A) B with KK = 32, M = N large), per precision.
-usage: tile_sweep.py [M] [KK]   (spawns one process per candidate, since
+usage: [TILES="0 1 8"] [KS="2"] tile_sweep.py [M] [KK]   (spawns one process per candidate, since
 MPCORE_GEMM_TILE is read once per process)"""
 import json, os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -13,7 +13,7 @@ def child(M, KK):
     L = nat.lib()
     dadd, _ = nat.fp64_peak()
     out = {}
-    for k in (2, 3, 4):
+    for k in [int(v) for v in os.environ.get("KS", "2 3 4").split()]:
         A = torch.rand(k, M, KK, dtype=torch.float64, device="cuda")
         B = torch.rand(k, KK, M, dtype=torch.float64, device="cuda")
         C = torch.rand(k, M, M, dtype=torch.float64, device="cuda")
@@ -39,7 +39,7 @@ if __name__ == "__main__":
     KK = int(sys.argv[2]) if len(sys.argv) > 2 else 32
     if os.environ.get("TILE_SWEEP_CHILD"):
         child(M, KK); sys.exit(0)
-    for i in range(6):
+    for i in [int(v) for v in os.environ.get("TILES", "0 1 2 3 4 5").split()]:
         env = dict(os.environ, MPCORE_GEMM_TILE=str(i), TILE_SWEEP_CHILD="1")
         r = subprocess.run([sys.executable, __file__, str(M), str(KK)], env=env,
                            capture_output=True, text=True)
