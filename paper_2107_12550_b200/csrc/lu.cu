@@ -222,7 +222,9 @@ swap_trsm_kernel(MatView A, int J, int w, int c0, int c1, int c2, int c3,
                  const int32_t *__restrict__ status) {
   // LPC lanes per column: 32 (one row per lane) or 16 (rows r and 31-r per
   // lane -- the triangle's shrinking work stays balanced, so a warp does
-  // 46 madd steps for two columns instead of 62)
+  // 46 madd steps for two columns instead of 62); the slot code below also
+  // takes LPC = 8 (four rows per lane, 19 steps per column), measured no
+  // faster than 16
   constexpr int CPW = 32 / LPC, CPB = 4 * CPW, NE = 2 * LU_MAX_W / LPC;
   if (threadIdx.x == 0) lu_stamp(J, 2, true);
   if (status[0] >= 0) return;
@@ -284,60 +286,62 @@ swap_trsm_kernel(MatView A, int J, int w, int c0, int c1, int c2, int c3,
     for (int k = 0; k < K; ++k)
       v[q][k] = ex[q] ? pc[k * A.plane + (int64_t)src[i] * ld] : 0.0;
   }
-  // rows of this lane: ra = sl, rb = 31 - sl (LPC = 16 only)
-  const int ra = sl, rb = LU_MAX_W - 1 - sl;
-  double ua[K], ub[K];
+  // rows of this lane, one per slot s: s LPC + sl for even s, s LPC +
+  // LPC - 1 - sl for odd s (LPC = 32: sl; 16: sl, 31 - sl; 8: sl, 15 - sl,
+  // 16 + sl, 31 - sl) -- every slot's rows shrink out of the triangle
+  // together, so the lanes stay balanced
+  constexpr int NS = LU_MAX_W / LPC;
+  int rr[NS];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    ua[k] = (live && right && ra < w) ? pc[k * A.plane + (int64_t)rsrc[ra] * ld]
-                                      : 0.0;
-    ub[k] = (LPC == 16 && live && right && rb < w)
-                ? pc[k * A.plane + (int64_t)rsrc[rb] * ld]
-                : 0.0;
-  }
+  for (int q = 0; q < NS; ++q)
+    rr[q] = (q & 1) ? q * LPC + LPC - 1 - sl : q * LPC + sl;
+  double u[NS][K];
+#pragma unroll
+  for (int q = 0; q < NS; ++q)
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      u[q][k] = (live && right && rr[q] < w)
+                    ? pc[k * A.plane + (int64_t)rsrc[rr[q]] * ld]
+                    : 0.0;
   __syncwarp();
   if (right) {
     for (int t = 0; t + 1 < w; ++t) {
-      // row t lives in slot a of sub-lane t (t < LPC), else in slot b of
-      // sub-lane 31 - t
-      const bool in_a = t < LPC;
-      const int srcl = gbase + (in_a ? t : LU_MAX_W - 1 - t);
+      // row t lives in slot t / LPC of the sub-lane holding it
+      const int st = t / LPC;
+      const int srcl =
+          gbase + ((st & 1) ? st * LPC + LPC - 1 - t : t - st * LPC);
       double ut[K];
 #pragma unroll
-      for (int k = 0; k < K; ++k)
-        ut[k] = __shfl_sync(0xffffffffu, in_a ? ua[k] : ub[k], srcl);
-      if (t < LPC - 1) {  // some row of slot a is still below t
-        double l[K], o[K];
+      for (int k = 0; k < K; ++k) {
+        double x = u[0][k];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          l[k] = Ls[k][ra][t];
-          o[k] = ua[k];
-        }
-        mc::madd<K>(o, l, ut);
-        const bool upd = ra > t && ra < w;
-#pragma unroll
-        for (int k = 0; k < K; ++k) ua[k] = upd ? o[k] : ua[k];
+        for (int q = 1; q < NS; ++q)
+          if (q == st) x = u[q][k];
+        ut[k] = __shfl_sync(0xffffffffu, x, srcl);
       }
-      if (LPC == 16) {
-        double l[K], o[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          l[k] = Ls[k][rb][t];
-          o[k] = ub[k];
+      for (int q = 0; q < NS; ++q) {
+        if (t < (q + 1) * LPC - 1) {  // some row of slot q is below t
+          double l[K], o[K];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            l[k] = Ls[k][rr[q]][t];
+            o[k] = u[q][k];
+          }
+          mc::madd<K>(o, l, ut);
+          const bool upd = rr[q] > t && rr[q] < w;
+#pragma unroll
+          for (int k = 0; k < K; ++k) u[q][k] = upd ? o[k] : u[q][k];
         }
-        mc::madd<K>(o, l, ut);
-        const bool upd = rb > t && rb < w;
-#pragma unroll
-        for (int k = 0; k < K; ++k) ub[k] = upd ? o[k] : ub[k];
       }
     }
-    if (live && ra < w) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) pc[k * A.plane + (int64_t)(J + ra) * ld] = ua[k];
-    }
-    if (LPC == 16 && live && rb < w) {
+    for (int q = 0; q < NS; ++q) {
+      if (live && rr[q] < w) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) pc[k * A.plane + (int64_t)(J + rb) * ld] = ub[k];
+        for (int k = 0; k < K; ++k)
+          pc[k * A.plane + (int64_t)(J + rr[q]) * ld] = u[q][k];
+      }
     }
   }
 #pragma unroll
@@ -467,6 +471,7 @@ cudaError_t lu_swap_trsm(int k, MatView A, int J, int w, int c0, int c1,
     const char *e = std::getenv("MPCORE_TRSM_PAIR_COLS");
     return e ? std::atoi(e) : 800;
   }();
+
   if (nl + nr == 0) return cudaSuccess;
   cudaError_t e = cudaSuccess;
   prof_begin(PROF_TRSM, s);
